@@ -1,0 +1,501 @@
+#!/usr/bin/env python
+"""Benchmark driver for the B200 recovery hot path (BASELINE.json metric:
+"Adam undo GB/s (% HBM peak); end-to-end recovery ms at 1/2/4/8 B200").
+
+A bench *step* = one inverse-step (optimizer_undo, optim.cpp:366-385) of the
+whole config-2 state: Adam on BERT-large (336,226,108 fp32 params, 398 groups,
+t=11 -> 10).  Between timed undos the state is re-stepped (untimed) so every
+undo inverts a real step.  value = algorithmic undo bytes (28 B/param: read
+x,g,m,v; write x,m,v) / CUDA-event time of the undo launches on their stream;
+inputs (9.4 GB) are far larger than L2, so no flush is needed.
+
+N>1 (torchrun): each rank undoes its own replica (weak scaling, no data-path
+collective); rank 0 additionally reports end-to-end replica recovery
+(resolve + undo + ncclBroadcast of the resolved GPT-2 XL state, config 3).
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified rewind optim.cpp built here) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BYTES_PER_ELEM_UNDO = {"adam": 28, "sgdm": 20}  # fp32 algorithmic (x,g,m,v r; x,m,v w)
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        rows = []
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(p[1]), smax=float(p[2]), pw=float(p[3]),
+                                 hw=p[5], hwt=p[6], swt=p[7], swp=p[8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [r for r in rows if r["pw"] > 250] or rows
+        reasons = set()
+        for r in loaded:
+            for k, name in (("hw", "hw_slowdown"), ("hwt", "hw_thermal_slowdown"),
+                            ("swt", "sw_thermal_slowdown"), ("swp", "sw_power_cap")):
+                if r[k].lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(r["sm"] for r in loaded),
+                "sm_max_mhz": max(r["smax"] for r in rows), "reasons": sorted(reasons),
+                "samples": len(rows), "samples_under_load": len(loaded),
+                "power_w_max": max(r["pw"] for r in rows)}
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return dict(hbm_gbs=d.get("hbm_gbs", 6650.0), src="measured")
+    return dict(hbm_gbs=6650.0, src="fallback")
+
+
+def _ncu_traffic(kernel_key: str):
+    """dram bytes per launch from a committed `ncu --set full` summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------- reference arm
+def cpu_reference_undo(seconds_target: float = 1.5, max_elems: int | None = None,
+                       threads: int | None = None, steps: int = 1, warmup: int = 0) -> dict:
+    """Time the reference optimizer_undo (oracle/_ref, fp64 as shipped) on the
+    host cores, block-parallel over groups (distinct blocks may run
+    concurrently).  Sample = the leading BERT-large groups summing to
+    a size that takes ~seconds_target per pass."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import ADAM, Ref
+    from paper_2302_06173_b200.workloads import bert_large_sizes
+
+    ref = Ref()
+    threads = threads or os.cpu_count() or 1
+    h = dict(kind=ADAM, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    sizes = bert_large_sizes()
+    # calibrate on ~4M elements
+    def make(sz_list):
+        blocks = []
+        for i, n in enumerate(sz_list):
+            b = ref.block(n, seed=i)
+            b.set(x=None, g=None, m=np.full(n, 1e-3), v=np.full(n, 1e-6), t=10, updated=False)
+            blocks.append((b, np.full(n, 1e-3)))
+        return blocks
+
+    def run(blocks, op):
+        def one(bg):
+            b, g = bg
+            if op == "step":
+                b.step(g, h)
+            else:
+                b.undo(h)
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, blocks))
+
+    cal_sizes, acc = [], 0
+    for n in sorted(sizes)[:]:
+        if acc > 4_000_000:
+            break
+        cal_sizes.append(n)
+        acc += n
+    cal = make(cal_sizes)
+    run(cal, "step")
+    t0 = time.perf_counter()
+    run(cal, "undo")
+    dt = max(time.perf_counter() - t0, 1e-6)
+    rate = acc / dt  # elems/s
+    want = int(rate * seconds_target)
+    if max_elems:
+        want = min(want, max_elems)
+    sample, acc2 = [], 0
+    for n in sizes:  # leading groups in layer order
+        if acc2 + n > want and sample:
+            continue
+        sample.append(n)
+        acc2 += n
+        if acc2 >= want:
+            break
+    del cal
+    blocks = make(sample)
+    times = []
+    for it in range(warmup + steps):
+        run(blocks, "step")
+        t0 = time.perf_counter()
+        run(blocks, "undo")
+        if it >= warmup:
+            times.append(time.perf_counter() - t0)
+    el = sum(sample)
+    sec = statistics.median(times)
+    return dict(value=el * 56 / sec / 1e9, unit="GB/s", cores=threads, kind="reference",
+                sample=f"rewind::optimizer_undo (oracle/_ref, fp64 as shipped) on the first "
+                       f"{len(sample)} BERT-large groups = {el} params, {threads} threads "
+                       f"block-parallel; GB/s counts the reference's own fp64 bytes "
+                       f"(56 B/param, 2x the fp32 config's 28 B/param)",
+                params=el, sec_per_pass=sec, params_per_s=el / sec,
+                fp32_equiv_gbs=el * 28 / sec / 1e9)
+
+
+def run_reference(args) -> None:
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return
+    steps, warmup = args.steps, args.warmup
+    t_start = time.perf_counter()
+    res = cpu_reference_undo(seconds_target=1.0, steps=steps, warmup=warmup)
+    line = {
+        "impl": "reference",
+        "metric": "Adam undo GB/s (% HBM peak); end-to-end recovery ms at 1/2/4/8 B200",
+        "value": round(res["value"], 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": steps,
+        "warmup": warmup, "ms_per_step": round(res["sec_per_pass"] * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded)",
+        "config": {"workload": "config 2: Adam undo, BERT-large 336M state (bounded sample)",
+                   "optimizer": "adam", "groups": 398, "params": 336226108},
+        "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "e2e": {"value": round(res["value"], 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "params_per_s": res["params_per_s"], "fp32_equiv_gbs": res["fp32_equiv_gbs"],
+        "wall_s": round(time.perf_counter() - t_start, 2),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- B200 arm
+def _fill_adam_state(st, seed=2302):
+    from paper_2302_06173_b200 import seeded_fill_
+    seeded_fill_(st.x, seed)
+    seeded_fill_(st.g, seed + 1)
+    seeded_fill_(st.m, seed + 2)
+    st.m.mul_(0.01)
+    seeded_fill_(st.v, seed + 3)
+    st.v.abs_().mul_(1e-4)
+
+
+def measure_undo(sizes, kind_name: str, steps: int, warmup: int, dtype=None, t0: int = 10):
+    """Device-resident undo timing: (per-undo ms list, bytes per undo, state)."""
+    import torch
+
+    from paper_2302_06173_b200 import ADAM, SGDM, DeviceState, OptimizerHyper
+    dtype = dtype or torch.float32
+    kind = ADAM if kind_name == "adam" else SGDM
+    st = DeviceState(sizes, dtype=dtype, kind=kind)
+    if kind == ADAM:
+        _fill_adam_state(st)
+        h = OptimizerHyper(kind=ADAM, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    else:
+        from paper_2302_06173_b200 import seeded_fill_
+        seeded_fill_(st.x, 1)
+        seeded_fill_(st.g, 2)
+        seeded_fill_(st.m, 3)
+        h = OptimizerHyper(kind=SGDM, lr=0.1, momentum=0.9, dampening=0.0, weight_decay=1e-4)
+    st.write_markers([(t0, 0)] * st.num_groups)
+    stream = torch.cuda.current_stream()
+    es = 8 if dtype == torch.float64 else 4
+    per_elem = (7 if kind == ADAM else 5) * es
+    nbytes = sum(sizes) * per_elem
+    for _ in range(warmup):
+        st.step(h)
+        st.undo(h)
+    torch.cuda.synchronize()
+    times = []
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for i in range(steps):
+        st.step(h)                       # re-arm (untimed)
+        evs[i][0].record(stream)
+        st.undo(h)                       # timed
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    times = [a.elapsed_time(b) for a, b in evs]
+    st.check_finite()
+    return times, nbytes, st, h
+
+
+def measure_e2e_host(st, h, steps: int):
+    """Same metric through the C-ABI with HOST buffers: each step copies the
+    state from pinned host memory, undoes it, and reads x, m, v back."""
+    import torch
+    stream = torch.cuda.current_stream()
+    hx = st.x.cpu().pin_memory()
+    hg = st.g.cpu().pin_memory()
+    hm = st.m.cpu().pin_memory()
+    hv = st.v.cpu().pin_memory()
+    ox, om, ov = (torch.empty_like(hx).pin_memory() for _ in range(3))
+    mk = st.markers()
+    armed = [(t, 1) for t, _ in mk]
+    h2d = sum(b.numel() * b.element_size() for b in (hx, hg, hm, hv))
+    d2h = sum(b.numel() * b.element_size() for b in (ox, om, ov))
+    times = []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        st.x.copy_(hx, non_blocking=True)
+        st.g.copy_(hg, non_blocking=True)
+        st.m.copy_(hm, non_blocking=True)
+        st.v.copy_(hv, non_blocking=True)
+        st.write_markers(armed)          # the host ParamBlocks arrive with updated=1
+        st.undo(h)
+        ox.copy_(st.x, non_blocking=True)
+        om.copy_(st.m, non_blocking=True)
+        ov.copy_(st.v, non_blocking=True)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        times.append(t0.elapsed_time(t1))
+    return times, h2d, d2h
+
+
+def recovery_e2e(world: int, rank: int, device, steps: int = 3):
+    """Config 3: replica recovery of a GPT-2 XL Adam state.  Rank 0 is the
+    survivor, crashed mid-update after half the groups (MidUpdate(G/2));
+    ranks 1..N-1 are replacements.  Timed: read markers + resolve (2
+    all-reduces) + undo + ncclBroadcast of x, m, v (+ markers)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper
+    from paper_2302_06173_b200.recovery import apply_resolution, recover_replication, resolve
+    from paper_2302_06173_b200.workloads import gpt2_xl_sizes
+    sizes = gpt2_xl_sizes()
+    st = DeviceState(sizes, kind=ADAM, device=device.index)
+    h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
+    if rank == 0:
+        _fill_adam_state(st)
+    res = []
+    for it in range(steps + 1):
+        if rank == 0:
+            st.write_markers([(10, 0)] * st.num_groups)
+            st.step(h, stop_after=st.num_groups // 2)   # crash mid-update
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t_wall = time.perf_counter()
+        e0.record()
+        if rank == 0:
+            mk = st.markers()
+            plan = resolve(mk, h, lens=sizes, device=device)
+            apply_resolution(st, h, plan)
+        else:  # replacements have no state: they join the consensus with nothing beyond it
+            plan = resolve([], h, device=device)
+        nbytes = recover_replication(st, src=0) if world > 1 else 0
+        e1.record()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t_wall) * 1e3
+        ms = e0.elapsed_time(e1)
+        if it > 0:
+            res.append((ms, wall, plan.strategy, plan.target, nbytes))
+    t = torch.tensor([max(r[1] for r in res)], device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    best = min(r[1] for r in res)
+    ms_med = statistics.median(r[1] for r in res)
+    nbytes = res[0][4]
+    del st
+    torch.cuda.empty_cache()
+    return dict(workload="config 3: GPT-2 XL (1,557,611,200 params, 580 groups) Adam fp32; "
+                         "rank 0 crashed after 290/580 groups; ranks 1..N-1 replacements",
+                recovery_ms_median=round(ms_med, 3), recovery_ms_best=round(best, 3),
+                recovery_ms_max_over_ranks=round(float(t.item()), 3), strategy=res[0][2],
+                target_iteration=res[0][3], bytes_per_replacement=nbytes,
+                broadcast_algbw_gbs=round(nbytes / (best * 1e-3) / 1e9, 2) if nbytes else None,
+                nvlink_roofline_ms=round(nbytes / 770e9 * 1e3, 3) if nbytes else None)
+
+
+def run_b200(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    if not torch.cuda.is_available():
+        print(json.dumps({"error": "no CUDA device; the B200 path has no CPU fallback"}))
+        sys.exit(1)
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    from paper_2302_06173_b200.workloads import CONFIGS
+    sizes = CONFIGS[args.config]["sizes"]()
+    kind_name = "sgdm" if args.config.startswith("sgdm") else "adam"
+    peaks = _peaks()
+    extras = {}
+    with ClockSampler(local) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        times, nbytes, st, h = measure_undo(sizes, kind_name, args.steps, args.warmup)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tot_ms = sum(times)
+        tmax = torch.tensor([tot_ms], device=device)
+        if world > 1:
+            dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tot_ms_max = float(tmax.item())
+        value = nbytes * args.steps * world / (tot_ms_max * 1e-3) / 1e9
+        mean_ms = tot_ms / args.steps
+        achieved = nbytes / (mean_ms * 1e-3) / 1e9
+        e2e_times, h2d, d2h = measure_e2e_host(st, h, max(1, min(args.steps, 3)))
+        e2e_ms = statistics.median(e2e_times)
+        e2e_val = nbytes * world / (e2e_ms * 1e-3) / 1e9
+        del st
+        torch.cuda.empty_cache()
+        if not args.no_extras and rank == 0 and world == 1:
+            t1b, nb1b, s1b, _ = measure_undo(CONFIGS["adam1b"]["sizes"](), "adam", 5, 2)
+            del s1b
+            torch.cuda.empty_cache()
+            m1 = statistics.median(t1b)
+            extras["adam1b_undo"] = dict(ms=round(m1, 4), gbs=round(nb1b / (m1 * 1e-3) / 1e9, 1),
+                                         frac_of_measured=round(nb1b / (m1 * 1e-3) / 1e9 /
+                                                                peaks["hbm_gbs"], 4),
+                                         frac_of_8tbs=round(nb1b / (m1 * 1e-3) / 8e12, 4),
+                                         target_ms=4.375, passes=m1 <= 4.375)
+            t64, nb64, s64, _ = measure_undo(sizes, "adam", 5, 2, dtype=torch.float64)
+            del s64
+            torch.cuda.empty_cache()
+            m64 = statistics.median(t64)
+            extras["adam340m_undo_f64"] = dict(ms=round(m64, 4),
+                                               gbs=round(nb64 / (m64 * 1e-3) / 1e9, 1))
+            tsg, nbsg, ssg, _ = measure_undo(CONFIGS["sgdm10m"]["sizes"](), "sgdm", 20, 3)
+            del ssg
+            msg = statistics.median(tsg)
+            extras["sgdm10m_undo_all"] = dict(ms=round(msg, 4),
+                                              gbs=round(nbsg / (msg * 1e-3) / 1e9, 1))
+        if not args.no_extras:
+            try:
+                extras["recovery"] = recovery_e2e(world, rank, device)
+            except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
+                extras["recovery"] = {"error": f"OOM: {e}"}
+    clocks = clk.summary()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            r = cpu_reference_undo(seconds_target=1.0, steps=3, warmup=1)
+            cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            cpu["params_per_s"] = r["params_per_s"]
+        except Exception as e:  # the oracle/_ref .so must have been built by build()
+            cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+    line = {
+        "metric": "Adam undo GB/s (% HBM peak); end-to-end recovery ms at 1/2/4/8 B200",
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(tot_ms_max / args.steps, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (device seeded_fill state, tensor.cpp:94-103)",
+        "config": {"workload": CONFIGS[args.config]["desc"], "optimizer": kind_name,
+                   "params": sum(sizes), "groups": len(sizes), "t": "11 -> 10",
+                   "bytes_per_param": BYTES_PER_ELEM_UNDO[kind_name],
+                   "l2": "inputs (9.4 GB) >> 126 MB L2; no flush needed",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                     "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                     "peak_source": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs, copy burst)",
+                     "frac_of_8tbs_spec": round(achieved / 8000.0, 4),
+                     "traffic": _ncu_traffic("adam_undo_f32_340m"),
+                     "kernel": "optim_kernel<float, ADAM, undo>"},
+        "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms": round(e2e_ms, 3),
+                "path": "C-ABI rw_optimizer_undo with pinned host buffers (H2D x,g,m,v; D2H x,m,v)"},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "extras": extras,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="adam340m", choices=["adam340m", "adam1b", "sgdm10m"])
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/*
+ * rewind_b200.h — C ABI of the B200-native Swift recovery hot path.
+ *
+ * Drop-in boundary for the reference's C++ operator API (`namespace rewind`,
+ * /root/reference/proj/core/include/rewind/ headers).  Every entry point names
+ * the reference interface it replaces.  Conventions:
+ *
+ *  - plain pointers and sizes only; no C++ or torch types cross this line;
+ *  - the caller owns all bulk device buffers (x, g, m, v, activations, ...);
+ *    the library only allocates its own small metadata (group table copy,
+ *    work lists) inside an rw_state and frees it in rw_state_destroy;
+ *  - every GPU call is stream-ordered and asynchronous on the given
+ *    cudaStream_t (passed as void*, NULL = legacy default stream);
+ *  - status codes: 0 = OK, otherwise 1 + (int)rewind::Err
+ *    (errors.hpp:11-33), so the C++ shim (rewind_b200.hpp) can rethrow the
+ *    exact rewind::Error the reference would have raised; 100+ are
+ *    B200-side failures (CUDA error, bad argument) with no reference twin;
+ *  - guards are checked in the reference's order BEFORE any mutation
+ *    (optim.cpp:340-348 for step, :367-370 plus the per-kind hyper checks for
+ *    undo); NumericalError is detected in-kernel (fused check_finite,
+ *    optim.cpp:361-363/:382-384) and reported after mutation by
+ *    rw_state_check(), exactly like the reference raises after mutating;
+ *  - thread-safe across distinct rw_state objects; one rw_state must not be
+ *    used from two host threads at once (one owner per block).
+ */
+#ifndef REWIND_B200_H
+#define REWIND_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RW_ABI_VERSION 1
+
+/* ---- status codes: 1 + rewind::Err (errors.hpp:11-33) ---- */
+enum {
+  RW_OK = 0,
+  RW_INVALID_SHAPE = 1,
+  RW_SHAPE_MISMATCH = 2,
+  RW_EMPTY_INPUT = 3,
+  RW_NUMERICAL_ERROR = 4,
+  RW_NON_INVERTIBLE_HYPER = 5,
+  RW_NOT_INVERTIBLE = 6,
+  RW_NOTHING_TO_UNDO = 7,
+  RW_ALREADY_UPDATED = 8,
+  RW_MISSING_ACTIVATION = 9,
+  RW_CHANNEL_BROKEN = 10,
+  RW_INVALID_INJECTION = 11,
+  RW_NOT_FAILED = 12,
+  RW_STORAGE_ERROR = 13,
+  RW_MISSING_LOG_DATA = 14,
+  RW_CORRUPT_LOG = 15,
+  RW_NO_CHECKPOINT = 16,
+  RW_NO_REPLICA = 17,
+  RW_INVALID_CONFIG = 18,
+  RW_TOO_LARGE = 19,
+  RW_CUDA_ERROR = 100,
+  RW_INVALID_ARGUMENT = 101
+};
+
+/* OptimizerKind, optim.hpp:16-23 (same order and values). */
+enum { RW_SGD = 0, RW_SGDM = 1, RW_ADAM = 2, RW_ADAMW = 3, RW_LAMB = 4, RW_AMSGRAD = 5 };
+/* Invertibility, optim.hpp:28. */
+enum { RW_INVERTIBLE = 0, RW_INVERTIBLE_WITH_SAVED_SCALARS = 1, RW_NOT_INVERTIBLE_KIND = 2 };
+/* element types of the flat state */
+enum { RW_F32 = 0, RW_F64 = 1 };
+
+/* OptimizerHyper, optim.hpp:34-50.  lr_table = (from_step, lr) breakpoints. */
+typedef struct rw_hyper {
+  int32_t kind;
+  int32_t require_invertible;
+  double lr;
+  double weight_decay; /* lambda */
+  double momentum;     /* mu  (SGD-momentum) */
+  double dampening;    /* tau (SGD-momentum) */
+  double beta1;
+  double beta2;
+  double eps;
+  const uint64_t* lr_table_from;
+  const double* lr_table_value;
+  uint32_t lr_table_len;
+  uint32_t _pad;
+} rw_hyper;
+
+/* One parameter group = one reference ParamBlock (optim.hpp:54-66) laid out
+ * inside the flat x/g/m/v buffers.  (t, updated) is the update-progress
+ * marker (optim.hpp:60-62); the kernels rewrite it in device memory when the
+ * last element of the group has been stored. */
+typedef struct rw_group {
+  uint64_t offset;  /* element offset into the flat buffers */
+  uint64_t len;     /* elements */
+  uint64_t t;       /* completed steps */
+  uint32_t updated; /* 1 = stepped in the current iteration */
+  uint32_t flags;   /* bit0: non-finite value produced by the last step/undo */
+} rw_group;
+
+typedef struct rw_state rw_state;
+
+/* ---- library ---- */
+int rw_abi_version(void);
+const char* rw_last_error_message(void); /* thread-local, message of the last failing call */
+const char* rw_status_name(int status);  /* err_name (errors.cpp:8-31) for 1..19 */
+int rw_device_count(void);
+
+/* invertibility_check(OptimizerKind), optim.hpp:32 / optim.cpp:113-126 */
+int rw_invertibility_check(int32_t kind);
+/* OptimizerHyper::validate, optim.cpp:137-149 */
+int rw_hyper_validate(const rw_hyper* h);
+/* OptimizerHyper::lr_at, optim.cpp:128-135 */
+int rw_lr_at(const rw_hyper* h, uint64_t t, double* out);
+
+/* ---- flat optimizer state (the device form of a set of ParamBlocks) ----
+ * x, g, m, v: caller-owned device buffers of `total` elements of `dtype`.
+ * m, v may be NULL for optimizers that do not use them (SGD; SGDM: v).
+ * vmax: AMSGrad running max (NULL otherwise).
+ * groups: n_groups host records (offset/len/t/updated) copied into a
+ * device-resident marker table owned by the state. */
+int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v,
+                    void* vmax, uint64_t total, const rw_group* groups, uint32_t n_groups,
+                    int32_t device);
+void rw_state_destroy(rw_state* s);
+uint32_t rw_state_num_groups(const rw_state* s);
+/* Copy the device marker table to `out` (n_groups records).  Synchronises
+ * `stream`.  The device table is authoritative after a crash-injected step. */
+int rw_state_read_groups(rw_state* s, rw_group* out, void* stream);
+/* Overwrite markers (host mirror and device table), e.g. when restoring a
+ * checkpoint or receiving a broadcast state. */
+int rw_state_write_groups(rw_state* s, const rw_group* in, void* stream);
+/* Synchronise `stream`; return RW_NUMERICAL_ERROR if any step/undo since the
+ * last check produced a non-finite x, m or v (and clear the flags). */
+int rw_state_check(rw_state* s, void* stream);
+/* End of iteration: clear the updated flag of the given groups (optim.hpp:62). */
+int rw_clear_updated(rw_state* s, const uint32_t* group_ids, uint32_t n, void* stream);
+/* Device pointers of the flat buffers (for collectives / copies). */
+void* rw_state_ptr(rw_state* s, int which /*0 x,1 g,2 m,3 v,4 vmax*/);
+
+/* optimizer_step(ParamBlock&, const Tensor& grad, const OptimizerHyper&),
+ * optim.hpp:71-72 / optim.cpp:338-364 — batched over `n` groups given in
+ * UPDATE ORDER (apply_layerwise_updates: reverse layer order).
+ * grad: flat device gradient in the same layout (NULL = g already holds it);
+ * the kernel caches it into g (optim.cpp:349) in the same pass.
+ * stop_after: crash injection MidUpdate(k): only the first
+ * min(n, stop_after) groups in update order are stepped; UINT32_MAX = all.
+ * Guards for ALL n groups are checked before anything is launched. */
+int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
+                      const void* grad, uint32_t stop_after, void* stream);
+
+/* optimizer_undo(ParamBlock&, const OptimizerHyper&), optim.hpp:76 /
+ * optim.cpp:366-385 — batched over `n` groups. */
+int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
+                      void* stream);
+
+/* ---- consistency resolver (no reference source) ---- */
+enum { RW_ACT_NONE = 0, RW_ACT_UNDO = 1, RW_ACT_REDO = 2 };
+enum { RW_POLICY_UNDO = 0 /* paper: always roll back to min */, RW_POLICY_MIN_COST = 1 };
+enum { RW_STRATEGY_NONE = 0, RW_STRATEGY_UNDO = 1, RW_STRATEGY_REDO = 2, RW_STRATEGY_GLOBAL_ROLLBACK = 3 };
+
+/* Per-rank summary exchanged with one MIN/MAX/SUM all-reduce each. */
+typedef struct rw_resolve_summary {
+  uint64_t t_min;          /* MIN over ranks: smallest group t (consensus_iteration) */
+  uint64_t t_max;          /* MAX over ranks: largest group t */
+  uint64_t undo_elems;     /* SUM-able: elements with t == t_min+1 (cost of undo) */
+  uint64_t redo_elems;     /* elements with t == t_min (cost of redo) */
+  uint64_t redo_blocked;   /* groups with t == t_min lacking a synchronised gradient */
+  uint64_t undo_blocked;   /* 1 if the optimizer/hyper cannot be undone */
+} rw_resolve_summary;
+
+/* Local summary of one rank's markers.  grad_ready[i] != 0 means group i's
+ * synchronised gradient for step t+1 has landed in the caller's gradient
+ * buffer (NULL = none ready).  Two phases: t_floor = UINT64_MAX gives the
+ * local t_min/t_max (all-reduce them MIN/MAX); then call again with
+ * t_floor = the global t_min to get costs/blocks relative to it (all-reduce
+ * the remaining fields with MAX). */
+int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad_ready,
+                         const rw_hyper* h, uint64_t t_floor, rw_resolve_summary* out);
+/* Given the all-reduced summary (t_min MIN, t_max MAX, the rest MAX), pick a
+ * strategy and target iteration, then the per-group actions for this rank. */
+int rw_resolve_plan(const rw_resolve_summary* global, int32_t policy, const rw_group* groups,
+                    uint32_t n, uint8_t* actions, uint64_t* target, int32_t* strategy);
+
+/* ---- numerics ---- */
+/* seeded_fill(shape, seed) (tensor.cpp:94-103) on the device, bit-identical to
+ * the host (fp64) / its single rounding (fp32).  offset = first counter index. */
+int rw_seeded_fill(int32_t dtype, void* out, uint64_t n, uint64_t seed, uint64_t offset,
+                   void* stream);
+uint64_t rw_derive_seed(uint64_t base, const uint64_t* parts, uint32_t n);
+/* ordered_sum (tensor.cpp:105-117): out = ((t0 + t1) + t2) + ...;
+ * tensors: host array of `count` device pointers of n elements. */
+int rw_ordered_sum(int32_t dtype, const void* const* tensors, uint32_t count, uint64_t n,
+                   void* out, void* stream);
+
+/* ---- selective-logging policy (planner.cpp missing) ---- */
+/* bubble_ratio(p, m), schedule.cpp:86-93 */
+int rw_bubble_ratio(int32_t p, int32_t m, int64_t* num, int64_t* den);
+/* group_machines(profile).  R[N] seconds, M[N-1] bytes per
+ * boundary per iteration, B bytes/s, T iterations, M_max bytes.
+ * group_of[N] receives each machine's group index; *n_groups the count;
+ * *storage = M(G), *recovery = expected recovery time per lost iteration. */
+int rw_group_machines(uint32_t N, const double* R, const double* M, double B, double T,
+                      double M_max, int32_t parallel, uint32_t* group_of, uint32_t* n_groups,
+                      double* storage, double* recovery);
+/* recovery_time_estimate(plan, lost_iterations) */
+int rw_recovery_time_estimate(uint32_t N, const double* R, const double* M, double B,
+                              int32_t parallel, const uint32_t* group_of,
+                              double lost_iterations, double* out);
+/* logging_worthwhile */
+int rw_logging_worthwhile(double bytes_per_iteration, double pcie_bytes_per_s, int32_t p,
+                          int32_t m, double iteration_time_s, int32_t* worthwhile,
+                          double* transfer_s, double* bubble_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REWIND_B200_H */

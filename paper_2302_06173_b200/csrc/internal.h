@@ -1,0 +1,65 @@
+// Internal declarations shared by the CUDA kernels and the C-ABI host code.
+// Not part of the public boundary (see include/rewind_b200.h).
+#pragma once
+#include <cstdint>
+
+#include "rewind_b200.h"
+
+namespace rwb {
+
+// Per selected group, per launch.  Built on the host in update order.
+struct WorkItem {
+  uint64_t off;          // element offset of the group in the flat buffers
+  uint64_t len;          // elements
+  uint64_t new_t;        // marker value written when the group completes
+  uint32_t gid;          // index into the device marker table
+  uint32_t chunk_begin;  // first global chunk index of this group
+  uint32_t nchunks;
+  uint32_t sidx;         // index into the ScalarSet table
+};
+
+// t-dependent scalars of one call, derived in double on the host exactly as
+// optim.cpp does (lr_at :128-135, bias_correction :172-175, denom :184/:255).
+struct ScalarSet {
+  double eta, c1, c2, denom;
+};
+
+// t-independent scalars (optim.cpp: 1.0 - h.beta1 etc. are double
+// expressions evaluated per element in the reference; they are loop
+// invariant so one host evaluation is the same value).
+struct Uniform {
+  double wd, mu, one_m_damp, b1, b2, one_m_b1, one_m_b2, eps;
+};
+
+struct LaunchArgs {
+  int dtype;     // RW_F32 / RW_F64
+  int kind;      // RW_SGD..RW_AMSGRAD
+  bool undo;
+  void* x;
+  void* g;
+  void* m;
+  void* v;
+  void* vmax;
+  const void* grad;  // step only; nullptr or == g means "g already holds it"
+  const WorkItem* work;
+  uint32_t n_work;
+  uint32_t total_chunks;
+  uint32_t chunk_elems;
+  const ScalarSet* sets;
+  Uniform u;
+  rw_group* groups;
+  uint32_t* done;
+};
+
+// record the thread-local last-error message (rw_last_error_message)
+void set_error(const char* msg);
+// elements per chunk for a dtype (one chunk = one CTA work unit)
+uint32_t chunk_elems_for(int dtype);
+// launch the fused step/undo kernel; returns cudaError_t as int
+int launch_optim(const LaunchArgs& a, void* stream);
+int launch_seeded_fill(int dtype, void* out, uint64_t n, uint64_t seed, uint64_t offset, void* stream);
+int launch_ordered_sum(int dtype, const void* const* tensors, uint32_t count, uint64_t n, void* out,
+                       void* stream);
+int launch_clear_updated(rw_group* groups, const uint32_t* ids, uint32_t n, void* stream);
+
+}  // namespace rwb

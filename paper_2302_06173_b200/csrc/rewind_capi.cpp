@@ -1,0 +1,549 @@
+// Host side of the C ABI (include/rewind_b200.h): guards, scalar derivation,
+// marker bookkeeping and launch of the fused kernels.  Mirrors the control
+// flow of optimizer_step / optimizer_undo (optim.cpp:338-385) group by group.
+//
+// Build note: compiled with -ffp-contract=off so the double scalars below are
+// the same IEEE expressions the reference evaluates (optim.cpp:172-175, :184,
+// :255) — glibc pow for the bias corrections, exactly as the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(RW_CUDA_ERROR, "CUDA error in %s: %s", what, cudaGetErrorString(e));
+}
+
+#define RW_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+const char* kErrNames[] = {"OK",           "InvalidShape",     "ShapeMismatch",  "EmptyInput",
+                           "NumericalError", "NonInvertibleHyper", "NotInvertible", "NothingToUndo",
+                           "AlreadyUpdated", "MissingActivation", "ChannelBroken", "InvalidInjection",
+                           "NotFailed",    "StorageError",     "MissingLogData", "CorruptLog",
+                           "NoCheckpoint", "NoReplica",        "InvalidConfig",  "TooLarge"};
+
+const char* kind_name(int k) {
+  switch (k) {
+    case RW_SGD: return "sgd";
+    case RW_SGDM: return "sgdm";
+    case RW_ADAM: return "adam";
+    case RW_ADAMW: return "adamw";
+    case RW_LAMB: return "lamb";
+    case RW_AMSGRAD: return "amsgrad";
+  }
+  return "?";
+}
+
+// OptimizerHyper::lr_at, optim.cpp:128-135
+int lr_at(const rw_hyper* h, uint64_t t, double* out) {
+  double v = h->lr;
+  for (uint32_t i = 0; i < h->lr_table_len; ++i)
+    if (t >= h->lr_table_from[i]) v = h->lr_table_value[i];
+  if (!(v > 0.0)) return fail(RW_INVALID_CONFIG, "InvalidConfig: learning rate must be positive");
+  *out = v;
+  return RW_OK;
+}
+
+// Ring of per-launch metadata slots so back-to-back asynchronous calls never
+// overwrite a work list that a queued copy/kernel still reads.
+struct Slot {
+  rwb::WorkItem* h_work = nullptr;  // pinned
+  rwb::ScalarSet* h_sets = nullptr; // pinned
+  rwb::WorkItem* d_work = nullptr;
+  rwb::ScalarSet* d_sets = nullptr;
+  uint32_t* d_done = nullptr;
+  uint32_t cap = 0;
+  uint32_t set_cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool used = false;
+};
+constexpr int kSlots = 8;
+
+}  // namespace
+
+namespace rwb {
+void set_error(const char* msg) { g_err = msg; }
+}  // namespace rwb
+
+struct rw_state {
+  int dtype = RW_F32;
+  int device = 0;
+  void* x = nullptr;
+  void* g = nullptr;
+  void* m = nullptr;
+  void* v = nullptr;
+  void* vmax = nullptr;
+  uint64_t total = 0;
+  std::vector<rw_group> mirror;  // host mirror of the marker table
+  rw_group* d_groups = nullptr;
+  Slot slots[kSlots];
+  int next_slot = 0;
+};
+
+namespace {
+
+int ensure_slot(rw_state* s, Slot& sl, uint32_t n_items, uint32_t n_sets) {
+  if (sl.used) RW_CUDA(cudaEventSynchronize(sl.ev));
+  if (!sl.ev) RW_CUDA(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+  if (n_items > sl.cap) {
+    cudaFreeHost(sl.h_work);
+    cudaFree(sl.d_work);
+    cudaFree(sl.d_done);
+    sl.h_work = nullptr;
+    sl.d_work = nullptr;
+    sl.d_done = nullptr;
+    uint32_t cap = std::max<uint32_t>(n_items, 256);
+    RW_CUDA(cudaMallocHost(&sl.h_work, sizeof(rwb::WorkItem) * cap));
+    RW_CUDA(cudaMalloc(&sl.d_work, sizeof(rwb::WorkItem) * cap));
+    RW_CUDA(cudaMalloc(&sl.d_done, sizeof(uint32_t) * cap));
+    RW_CUDA(cudaMemset(sl.d_done, 0, sizeof(uint32_t) * cap));
+    sl.cap = cap;
+  }
+  if (n_sets > sl.set_cap) {
+    cudaFreeHost(sl.h_sets);
+    cudaFree(sl.d_sets);
+    uint32_t cap = std::max<uint32_t>(n_sets, 16);
+    RW_CUDA(cudaMallocHost(&sl.h_sets, sizeof(rwb::ScalarSet) * cap));
+    RW_CUDA(cudaMalloc(&sl.d_sets, sizeof(rwb::ScalarSet) * cap));
+    sl.set_cap = cap;
+  }
+  (void)s;
+  return RW_OK;
+}
+
+rwb::Uniform uniform_of(const rw_hyper* h) {
+  rwb::Uniform u;
+  u.wd = h->weight_decay;
+  u.mu = h->momentum;
+  u.one_m_damp = 1.0 - h->dampening;
+  u.b1 = h->beta1;
+  u.b2 = h->beta2;
+  u.one_m_b1 = 1.0 - h->beta1;
+  u.one_m_b2 = 1.0 - h->beta2;
+  u.eps = h->eps;
+  return u;
+}
+
+// Build the scalar set for the step/undo index tt (the t the reference feeds
+// lr_at and bias_correction).
+rwb::ScalarSet scalars_at(const rw_hyper* h, uint64_t tt, double eta) {
+  rwb::ScalarSet ss;
+  ss.eta = eta;
+  ss.c1 = 1.0 - std::pow(h->beta1, static_cast<double>(tt));
+  ss.c2 = 1.0 - std::pow(h->beta2, static_cast<double>(tt));
+  ss.denom = 1.0 - eta * h->weight_decay;
+  return ss;
+}
+
+int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, bool undo,
+                  const void* grad, const std::vector<double>& etas, void* stream) {
+  if (n == 0) return RW_OK;
+  RW_CUDA(cudaSetDevice(s->device));
+  Slot& sl = s->slots[s->next_slot];
+  s->next_slot = (s->next_slot + 1) % kSlots;
+
+  // distinct scalar sets by tt
+  std::map<uint64_t, uint32_t> set_of;
+  for (uint32_t i = 0; i < n; ++i) {
+    const rw_group& gr = s->mirror[ids[i]];
+    const uint64_t tt = undo ? gr.t : gr.t + 1;
+    set_of.emplace(tt, 0);
+  }
+  int st = ensure_slot(s, sl, n, static_cast<uint32_t>(set_of.size()));
+  if (st) return st;
+  {
+    uint32_t k = 0;
+    for (auto& kv : set_of) kv.second = k++;
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    const rw_group& gr = s->mirror[ids[i]];
+    const uint64_t tt = undo ? gr.t : gr.t + 1;
+    sl.h_sets[set_of[tt]] = scalars_at(h, tt, etas[i]);
+  }
+  const uint32_t ce = rwb::chunk_elems_for(s->dtype);
+  uint64_t chunk = 0;
+  uint32_t n_items = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    const rw_group& gr = s->mirror[ids[i]];
+    rwb::WorkItem& w = sl.h_work[n_items++];
+    w.off = gr.offset;
+    w.len = gr.len;
+    w.gid = ids[i];
+    w.new_t = undo ? gr.t - 1 : gr.t + 1;
+    w.nchunks = static_cast<uint32_t>((gr.len + ce - 1) / ce);
+    w.chunk_begin = static_cast<uint32_t>(chunk);
+    w.sidx = set_of[undo ? gr.t : gr.t + 1];
+    chunk += w.nchunks;
+  }
+  if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one call");
+  auto cs = static_cast<cudaStream_t>(stream);
+  if (n_items > 0) {
+    RW_CUDA(cudaMemcpyAsync(sl.d_work, sl.h_work, sizeof(rwb::WorkItem) * n_items,
+                            cudaMemcpyHostToDevice, cs));
+    RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * set_of.size(),
+                            cudaMemcpyHostToDevice, cs));
+    rwb::LaunchArgs a;
+    a.dtype = s->dtype;
+    a.kind = h->kind;
+    a.undo = undo;
+    a.x = s->x;
+    a.g = s->g;
+    a.m = s->m;
+    a.v = s->v;
+    a.vmax = s->vmax;
+    a.grad = grad;
+    a.work = sl.d_work;
+    a.n_work = n_items;
+    a.total_chunks = static_cast<uint32_t>(chunk);
+    a.chunk_elems = ce;
+    a.sets = sl.d_sets;
+    a.u = uniform_of(h);
+    a.groups = s->d_groups;
+    a.done = sl.d_done;
+    int e = rwb::launch_optim(a, stream);
+    if (e) return cuda_fail(static_cast<cudaError_t>(e), "optim kernel launch");
+  }
+  // host mirror follows what the kernel writes at group completion
+  for (uint32_t i = 0; i < n; ++i) {
+    rw_group& gr = s->mirror[ids[i]];
+    gr.t = undo ? gr.t - 1 : gr.t + 1;
+    gr.updated = undo ? 0u : 1u;
+  }
+  RW_CUDA(cudaEventRecord(sl.ev, cs));
+  sl.used = true;
+  return RW_OK;
+}
+
+size_t elem_size(int dtype) { return dtype == RW_F64 ? 8 : 4; }
+
+}  // namespace
+
+extern "C" {
+
+int rw_abi_version(void) { return RW_ABI_VERSION; }
+const char* rw_last_error_message(void) { return g_err.c_str(); }
+const char* rw_status_name(int status) {
+  if (status >= 0 && status <= 19) return kErrNames[status];
+  if (status == RW_CUDA_ERROR) return "CudaError";
+  if (status == RW_INVALID_ARGUMENT) return "InvalidArgument";
+  return "Unknown";
+}
+int rw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int rw_invertibility_check(int32_t kind) {
+  switch (kind) {
+    case RW_SGD:
+    case RW_SGDM:
+    case RW_ADAM:
+    case RW_ADAMW: return RW_INVERTIBLE;
+    case RW_LAMB: return RW_INVERTIBLE_WITH_SAVED_SCALARS;
+    default: return RW_NOT_INVERTIBLE_KIND;
+  }
+}
+
+// OptimizerHyper::validate, optim.cpp:137-149 (same checks, same order)
+int rw_hyper_validate(const rw_hyper* h) {
+  if (!h) return fail(RW_INVALID_ARGUMENT, "null hyper");
+  if (!(h->lr > 0.0)) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.lr must be > 0");
+  if (h->weight_decay < 0.0) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.weight_decay must be >= 0");
+  if (h->momentum < 0.0 || h->momentum > 1.0) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.momentum must be in [0,1]");
+  if (h->dampening < 0.0 || h->dampening > 1.0) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.dampening must be in [0,1]");
+  if (h->beta1 < 0.0 || h->beta1 >= 1.0) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.beta1 must be in [0,1)");
+  if (h->beta2 < 0.0 || h->beta2 >= 1.0) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.beta2 must be in [0,1)");
+  if (!(h->eps > 0.0)) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.eps must be > 0");
+  for (uint32_t i = 0; i < h->lr_table_len; ++i)
+    if (!(h->lr_table_value[i] > 0.0)) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.lr_table entries must be > 0");
+  return RW_OK;
+}
+
+int rw_lr_at(const rw_hyper* h, uint64_t t, double* out) {
+  if (!h || !out) return fail(RW_INVALID_ARGUMENT, "null argument");
+  return lr_at(h, t, out);
+}
+
+int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v, void* vmax,
+                    uint64_t total, const rw_group* groups, uint32_t n_groups, int32_t device) {
+  if (!out) return fail(RW_INVALID_ARGUMENT, "null out");
+  *out = nullptr;
+  if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "dtype must be RW_F32 or RW_F64");
+  if (!x || !g) return fail(RW_INVALID_ARGUMENT, "x and g are required");
+  for (void* p : {x, g, m, v, vmax})
+    if (p && (reinterpret_cast<uintptr_t>(p) & 15u))
+      return fail(RW_INVALID_ARGUMENT, "state buffers must be 16-byte aligned");
+  if (n_groups > 0 && !groups) return fail(RW_INVALID_ARGUMENT, "null groups");
+  for (uint32_t i = 0; i < n_groups; ++i) {
+    // shape_elements (tensor.cpp:125-133): a zero extent is InvalidShape
+    if (groups[i].len == 0) return fail(RW_INVALID_SHAPE, "InvalidShape: zero extent (group %u)", i);
+    if (groups[i].offset + groups[i].len > total || groups[i].offset + groups[i].len < groups[i].offset)
+      return fail(RW_INVALID_SHAPE, "InvalidShape: group %u [%llu, +%llu) exceeds the state (%llu)", i,
+                  (unsigned long long)groups[i].offset, (unsigned long long)groups[i].len,
+                  (unsigned long long)total);
+  }
+  int ndev = rw_device_count();
+  if (ndev == 0) return fail(RW_CUDA_ERROR, "no CUDA device visible: the B200 path has no CPU fallback");
+  if (device < 0 || device >= ndev) return fail(RW_INVALID_ARGUMENT, "bad device %d", device);
+  auto* s = new rw_state();
+  s->dtype = dtype;
+  s->device = device;
+  s->x = x;
+  s->g = g;
+  s->m = m;
+  s->v = v;
+  s->vmax = vmax;
+  s->total = total;
+  s->mirror.assign(groups, groups + n_groups);
+  for (auto& gr : s->mirror) gr.flags = 0;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_groups, sizeof(rw_group) * n_groups);
+  if (e == cudaSuccess && n_groups)
+    e = cudaMemcpy(s->d_groups, s->mirror.data(), sizeof(rw_group) * n_groups, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    rw_state_destroy(s);
+    return cuda_fail(e, "rw_state_create");
+  }
+  *out = s;
+  return RW_OK;
+}
+
+void rw_state_destroy(rw_state* s) {
+  if (!s) return;
+  cudaSetDevice(s->device);
+  for (auto& sl : s->slots) {
+    if (sl.ev) {
+      cudaEventSynchronize(sl.ev);
+      cudaEventDestroy(sl.ev);
+    }
+    cudaFreeHost(sl.h_work);
+    cudaFreeHost(sl.h_sets);
+    cudaFree(sl.d_work);
+    cudaFree(sl.d_sets);
+    cudaFree(sl.d_done);
+  }
+  cudaFree(s->d_groups);
+  delete s;
+}
+
+uint32_t rw_state_num_groups(const rw_state* s) { return s ? static_cast<uint32_t>(s->mirror.size()) : 0; }
+
+void* rw_state_ptr(rw_state* s, int which) {
+  if (!s) return nullptr;
+  switch (which) {
+    case 0: return s->x;
+    case 1: return s->g;
+    case 2: return s->m;
+    case 3: return s->v;
+    case 4: return s->vmax;
+  }
+  return nullptr;
+}
+
+int rw_state_read_groups(rw_state* s, rw_group* out, void* stream) {
+  if (!s || !out) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (s->mirror.empty()) return RW_OK;
+  RW_CUDA(cudaSetDevice(s->device));
+  auto cs = static_cast<cudaStream_t>(stream);
+  RW_CUDA(cudaMemcpyAsync(out, s->d_groups, sizeof(rw_group) * s->mirror.size(), cudaMemcpyDeviceToHost, cs));
+  RW_CUDA(cudaStreamSynchronize(cs));
+  // device table is authoritative
+  for (size_t i = 0; i < s->mirror.size(); ++i) {
+    s->mirror[i].t = out[i].t;
+    s->mirror[i].updated = out[i].updated;
+  }
+  return RW_OK;
+}
+
+int rw_state_write_groups(rw_state* s, const rw_group* in, void* stream) {
+  if (!s || !in) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (s->mirror.empty()) return RW_OK;
+  for (size_t i = 0; i < s->mirror.size(); ++i) {
+    if (in[i].offset != s->mirror[i].offset || in[i].len != s->mirror[i].len)
+      return fail(RW_SHAPE_MISMATCH, "ShapeMismatch: group %zu layout differs", i);
+  }
+  RW_CUDA(cudaSetDevice(s->device));
+  s->mirror.assign(in, in + s->mirror.size());
+  auto cs = static_cast<cudaStream_t>(stream);
+  RW_CUDA(cudaMemcpyAsync(s->d_groups, s->mirror.data(), sizeof(rw_group) * s->mirror.size(),
+                          cudaMemcpyHostToDevice, cs));
+  RW_CUDA(cudaStreamSynchronize(cs));
+  return RW_OK;
+}
+
+int rw_state_check(rw_state* s, void* stream) {
+  if (!s) return fail(RW_INVALID_ARGUMENT, "null state");
+  if (s->mirror.empty()) return RW_OK;
+  std::vector<rw_group> dev(s->mirror.size());
+  int st = rw_state_read_groups(s, dev.data(), stream);
+  if (st) return st;
+  bool bad = false;
+  uint32_t first = 0;
+  for (size_t i = 0; i < dev.size(); ++i)
+    if (dev[i].flags & 1u) {
+      if (!bad) first = static_cast<uint32_t>(i);
+      bad = true;
+      dev[i].flags &= ~1u;
+    }
+  if (!bad) return RW_OK;
+  auto cs = static_cast<cudaStream_t>(stream);
+  RW_CUDA(cudaMemcpyAsync(s->d_groups, dev.data(), sizeof(rw_group) * dev.size(), cudaMemcpyHostToDevice, cs));
+  RW_CUDA(cudaStreamSynchronize(cs));
+  return fail(RW_NUMERICAL_ERROR, "NumericalError: non-finite value in optimizer state (group %u)", first);
+}
+
+int rw_clear_updated(rw_state* s, const uint32_t* ids, uint32_t n, void* stream) {
+  if (!s) return fail(RW_INVALID_ARGUMENT, "null state");
+  for (uint32_t i = 0; i < n; ++i) {
+    if (ids[i] >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", ids[i]);
+    s->mirror[ids[i]].updated = 0;
+  }
+  RW_CUDA(cudaSetDevice(s->device));
+  int e = rwb::launch_clear_updated(s->d_groups, ids, n, stream);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "clear_updated");
+  return RW_OK;
+}
+
+// optimizer_step, optim.cpp:338-364
+int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n,
+                      const void* grad, uint32_t stop_after, void* stream) {
+  if (!s || !h || (n && !ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (n > stop_after) n = stop_after;  // MidUpdate(k): the crash hits after k groups
+  std::vector<double> etas(n);
+  std::vector<uint8_t> seen(s->mirror.size(), 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (ids[i] >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", ids[i]);
+    if (seen[ids[i]]) return fail(RW_INVALID_ARGUMENT, "group id %u listed twice", ids[i]);
+    seen[ids[i]] = 1;
+    const rw_group& gr = s->mirror[ids[i]];
+    // require_same_shape (:340) holds by construction: grad shares the flat layout.
+    if (gr.updated) return fail(RW_ALREADY_UPDATED, "AlreadyUpdated: block already stepped this iteration (group %u)", ids[i]);
+    if (h->require_invertible && rw_invertibility_check(h->kind) == RW_NOT_INVERTIBLE_KIND)
+      return fail(RW_NOT_INVERTIBLE, "NotInvertible: %s cannot be undone", kind_name(h->kind));
+    // :349 caches the gradient BEFORE :350 lr_at may raise; reproduce that
+    // partial mutation for the failing group only.
+    int st = lr_at(h, gr.t + 1, &etas[i]);
+    if (st) {
+      if (grad && grad != s->g) {
+        const size_t es = elem_size(s->dtype);
+        auto cs = static_cast<cudaStream_t>(stream);
+        RW_CUDA(cudaMemcpyAsync(static_cast<char*>(s->g) + gr.offset * es,
+                                static_cast<const char*>(grad) + gr.offset * es, gr.len * es,
+                                cudaMemcpyDeviceToDevice, cs));
+      }
+      return st;
+    }
+  }
+  if (h->kind == RW_LAMB)
+    return fail(RW_INVALID_ARGUMENT, "lamb step is not on the B200 path yet (SURVEY §8f rank 2)");
+  if (h->kind == RW_AMSGRAD && !s->vmax) return fail(RW_INVALID_ARGUMENT, "amsgrad needs a vmax buffer");
+  if ((h->kind != RW_SGD && !s->m) ||
+      ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_AMSGRAD) && !s->v))
+    return fail(RW_INVALID_ARGUMENT, "%s needs m%s buffers", kind_name(h->kind),
+                h->kind == RW_SGDM ? "" : " and v");
+  return launch_groups(s, h, ids, n, false, grad, etas, stream);
+}
+
+// optimizer_undo, optim.cpp:366-385 and the per-kind guards of undo_<kind>
+int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, void* stream) {
+  if (!s || !h || (n && !ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
+  std::vector<double> etas(n);
+  std::vector<uint8_t> seen(s->mirror.size(), 0);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (ids[i] >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", ids[i]);
+    if (seen[ids[i]]) return fail(RW_INVALID_ARGUMENT, "group id %u listed twice", ids[i]);
+    seen[ids[i]] = 1;
+    const rw_group& gr = s->mirror[ids[i]];
+    if (!gr.updated) return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: block has no pending update (group %u)", ids[i]);
+    if (h->kind == RW_AMSGRAD) return fail(RW_NOT_INVERTIBLE, "NotInvertible: amsgrad element-wise max has no inverse");
+    int st = lr_at(h, gr.t, &etas[i]);
+    if (st) return st;
+    const double eta = etas[i];
+    switch (h->kind) {
+      case RW_SGD:  // optim.cpp:184-185
+        if (1.0 - eta * h->weight_decay == 0.0)
+          return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1 for sgd");
+        break;
+      case RW_SGDM:  // :200
+        if (h->momentum == 0.0) return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: momentum == 0 for sgdm");
+        break;
+      case RW_ADAM:  // :222-224
+        if (h->beta1 == 0.0 || h->beta2 == 0.0)
+          return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for adam");
+        break;
+      case RW_ADAMW:  // :252-256
+        if (h->beta1 == 0.0 || h->beta2 == 0.0)
+          return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for adamw");
+        if (1.0 - eta * h->weight_decay == 0.0)
+          return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1 for adamw");
+        break;
+      case RW_LAMB:
+        if (h->beta1 == 0.0 || h->beta2 == 0.0)
+          return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for lamb");
+        return fail(RW_INVALID_ARGUMENT, "lamb undo is not on the B200 path yet (SURVEY §8f rank 2)");
+      default: return fail(RW_INVALID_ARGUMENT, "unknown optimizer kind %d", h->kind);
+    }
+  }
+  if ((h->kind != RW_SGD && !s->m) || ((h->kind == RW_ADAM || h->kind == RW_ADAMW) && !s->v))
+    return fail(RW_INVALID_ARGUMENT, "%s needs m/v buffers", kind_name(h->kind));
+  return launch_groups(s, h, ids, n, true, nullptr, etas, stream);
+}
+
+// ---------------- numerics ----------------
+static uint64_t mix64(uint64_t x) {  // tensor.cpp:69-74
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+uint64_t rw_derive_seed(uint64_t base, const uint64_t* parts, uint32_t n) {  // tensor.cpp:76-83
+  uint64_t h = mix64(base);
+  for (uint32_t i = 0; i < n; ++i) h = mix64(h ^ mix64(parts[i]));
+  return h;
+}
+int rw_seeded_fill(int32_t dtype, void* out, uint64_t n, uint64_t seed, uint64_t offset, void* stream) {
+  if (!out && n) return fail(RW_INVALID_ARGUMENT, "null out");
+  int e = rwb::launch_seeded_fill(dtype, out, n, seed, offset, stream);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "seeded_fill");
+  return RW_OK;
+}
+int rw_ordered_sum(int32_t dtype, const void* const* tensors, uint32_t count, uint64_t n, void* out,
+                   void* stream) {
+  if (count == 0) return fail(RW_EMPTY_INPUT, "EmptyInput: ordered_sum of nothing");
+  int e = rwb::launch_ordered_sum(dtype, tensors, count, n, out, stream);
+  if (e) return cuda_fail(static_cast<cudaError_t>(e), "ordered_sum");
+  return RW_OK;
+}
+
+}  // extern "C"

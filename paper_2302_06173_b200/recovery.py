@@ -1,0 +1,147 @@
+"""Recovery orchestration: consistency resolver + replica recovery.
+
+Reference contracts (recovery.cpp is absent):
+  * consensus_iteration  SPEC:475-483  (min over survivors)
+  * apply_undo           SPEC:484-492  (undo blocks beyond the target)
+  * recover_replication  SPEC:493-501  (bit-exact copy of the survivor state)
+
+One process per GPU.  ``torch.distributed`` is the plumbing: NCCL over
+NVLink on the B200 box (the MIN/MAX all-reduces of the resolver and the
+ncclBroadcast of the resolved state), gloo in the CPU tests of the host
+logic.  The per-group decisions are made by the C++ resolver
+(csrc/resolver_planner.cpp) and the arithmetic by the fused CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+import torch.distributed as dist
+
+from ._lib import (ACT_REDO, ACT_UNDO, LIB, POLICY_MIN_COST, POLICY_UNDO, STRATEGY_GLOBAL_ROLLBACK,
+                   STRATEGY_NAMES, STRATEGY_REDO, STRATEGY_UNDO, RwError, check, rw_group, rw_hyper,
+                   rw_resolve_summary)
+
+U64_MAX = 2**64 - 1
+
+
+@dataclass
+class ResolvePlan:
+    strategy: str
+    target: int
+    actions: list[int]                  # per local group: 0 none, 1 undo, 2 redo
+    summary: dict = field(default_factory=dict)
+
+    @property
+    def undo_ids(self) -> list[int]:
+        return [i for i, a in enumerate(self.actions) if a == ACT_UNDO]
+
+    @property
+    def redo_ids(self) -> list[int]:
+        return [i for i, a in enumerate(self.actions) if a == ACT_REDO]
+
+
+def _groups_from_markers(markers: Sequence[tuple[int, int]], lens: Sequence[int] | None = None):
+    g = (rw_group * max(len(markers), 1))()
+    for i, (t, u) in enumerate(markers):
+        g[i].offset, g[i].len = 0, (lens[i] if lens is not None else 1)
+        g[i].t, g[i].updated, g[i].flags = t, u, 0
+    return g
+
+
+def _allreduce_u64(vals: list[int], op, group=None, device=None) -> list[int]:
+    """All-reduce a few uint64 counters (sent as int64; values < 2^63)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return list(vals)
+    backend = dist.get_backend(group)
+    dev = device if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([int(v) for v in vals], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=op, group=group)
+    return [int(v) for v in t.cpu().tolist()]
+
+
+def resolve(markers: Sequence[tuple[int, int]], hyper, lens: Sequence[int] | None = None,
+            grad_ready: Sequence[bool] | None = None, policy: str = "undo", group=None,
+            device=None) -> ResolvePlan:
+    """Consensus + per-group undo/redo decision across all survivor ranks.
+
+    markers: this rank's (t, updated) per group (read from the device table).
+    Exchanges: one MIN/MAX all-reduce of (t_min, t_max), one MAX all-reduce of
+    the costs / blocks relative to the global t_min.
+    """
+    h: rw_hyper = hyper.to_c() if hasattr(hyper, "to_c") else hyper
+    g = _groups_from_markers(markers, lens)
+    n = len(markers)
+    ready = None
+    if grad_ready is not None:
+        ready = (C.c_uint8 * max(n, 1))(*[1 if r else 0 for r in grad_ready])
+    loc = rw_resolve_summary()
+    check(LIB.rw_resolve_summarize(g, n, ready, C.byref(h), U64_MAX, C.byref(loc)))
+    t_min = loc.t_min if n else U64_MAX >> 1
+    lo = _allreduce_u64([t_min], dist.ReduceOp.MIN if dist.is_available() else None, group, device)[0]
+    hi = _allreduce_u64([loc.t_max], dist.ReduceOp.MAX if dist.is_available() else None, group,
+                        device)[0]
+    s2 = rw_resolve_summary()
+    check(LIB.rw_resolve_summarize(g, n, ready, C.byref(h), lo, C.byref(s2)))
+    costs = _allreduce_u64([s2.undo_elems, s2.redo_elems, s2.redo_blocked, s2.undo_blocked],
+                           dist.ReduceOp.MAX if dist.is_available() else None, group, device)
+    glob = rw_resolve_summary()
+    glob.t_min, glob.t_max = lo, hi
+    glob.undo_elems, glob.redo_elems, glob.redo_blocked, glob.undo_blocked = costs
+    acts = (C.c_uint8 * max(n, 1))()
+    tgt, st = C.c_uint64(), C.c_int32()
+    pol = POLICY_MIN_COST if policy == "min_cost" else POLICY_UNDO
+    check(LIB.rw_resolve_plan(C.byref(glob), pol, g, n, acts, C.byref(tgt), C.byref(st)))
+    return ResolvePlan(STRATEGY_NAMES[st.value], tgt.value, list(acts[:n]),
+                       dict(t_min=lo, t_max=hi, undo_elems=costs[0], redo_elems=costs[1],
+                            redo_blocked=costs[2], undo_blocked=costs[3]))
+
+
+def apply_resolution(state, hyper, plan: ResolvePlan, grad: torch.Tensor | None = None,
+                     stream=None) -> None:
+    """Execute a ResolvePlan on a DeviceState with the fused kernels.
+
+    Undo: groups beyond the target whose updated flag was already cleared
+    (completed iteration) are re-armed first — the spec gap of SURVEY §8a
+    row a13: the decision is on t, at most one step back, g still caches that
+    step's gradient (one version kept).
+    Redo: lagging groups are stepped with their synchronised gradient `grad`.
+    """
+    if plan.strategy == STRATEGY_NAMES[STRATEGY_GLOBAL_ROLLBACK]:
+        raise RwError(101, "plan requires a global checkpoint rollback (SPEC:488)")
+    if plan.strategy == STRATEGY_NAMES[STRATEGY_UNDO] and plan.undo_ids:
+        mk = state.markers(stream)
+        if any(mk[i][1] == 0 for i in plan.undo_ids):
+            state.write_markers([(t, 1 if i in set(plan.undo_ids) else u)
+                                 for i, (t, u) in enumerate(mk)], stream)
+        # undo in reverse update order (first layer's update was the last)
+        order = [i for i in reversed(state.update_order()) if i in set(plan.undo_ids)]
+        state.undo(hyper, order, stream=stream)
+    elif plan.strategy == STRATEGY_NAMES[STRATEGY_REDO] and plan.redo_ids:
+        if grad is None:
+            raise RwError(101, "redo needs the synchronised gradient buffer")
+        order = [i for i in state.update_order() if i in set(plan.redo_ids)]
+        state.step(hyper, order, grad=grad, stream=stream)
+
+
+def recover_replication(state, src: int, include_grad: bool = False, group=None) -> int:
+    """recover_replication: broadcast the resolved state from the
+    surviving rank `src` to every other rank of `group` (NCCL over NVLink).
+    Bit-exact copy semantics; markers travel with it.  Returns bytes received
+    per replacement."""
+    if not (dist.is_available() and dist.is_initialized()):
+        raise RwError(17, "NoReplica: no process group")
+    bufs = [state.x] + ([state.g] if include_grad else [])
+    bufs += [b for b in (state.m, state.v) if b is not None]
+    for b in bufs:
+        dist.broadcast(b, src=src, group=group)
+    mk = state.markers()
+    backend = dist.get_backend(group)
+    dev = state.device if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([v for pair in mk for v in pair], dtype=torch.int64, device=dev)
+    dist.broadcast(t, src=src, group=group)
+    flat = t.cpu().tolist()
+    state.write_markers([(flat[2 * i], flat[2 * i + 1]) for i in range(len(mk))])
+    return sum(b.numel() * b.element_size() for b in bufs)

@@ -1,0 +1,274 @@
+"""GPU parity of the fused step/undo kernels (through the C ABI).
+
+Bars (north_star):
+  * fp64 kernels: bit-exact vs the reference library (golden fixtures from
+    oracle/_ref and the live fp64 restatement, itself pinned bit-exact to _ref);
+  * fp32 kernels: bit-exact vs the fp32 restatement (reference operation order
+    in float, no FMA contraction);
+  * markers, guards and error codes identical to optimizer_step/undo.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import Restate
+from paper_2302_06173_b200 import (ADAM, ADAMW, AMSGRAD, SGD, SGDM, DeviceState, OptimizerHyper,
+                                   RwError, ordered_sum, seeded_fill_)
+
+pytestmark = pytest.mark.gpu
+
+F = float.fromhex
+HYP = {
+    SGD: OptimizerHyper(kind=SGD, lr=0.05, weight_decay=0.01),
+    SGDM: OptimizerHyper(kind=SGDM, lr=0.1, momentum=0.9, dampening=0.1, weight_decay=1e-4),
+    ADAM: OptimizerHyper(kind=ADAM, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01),
+    ADAMW: OptimizerHyper(kind=ADAMW, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01),
+}
+NAMES = {"sgd": SGD, "sgdm": SGDM, "adam": ADAM, "adamw": ADAMW}
+
+
+def _bits(a):
+    a = np.asarray(a)
+    return a.view(np.uint64 if a.dtype == np.float64 else np.uint32)
+
+
+def _load(st: DeviceState, i, x, g, m, v):
+    dt = st.dtype
+    st.view("x", i).copy_(torch.as_tensor(x, dtype=dt))
+    st.view("g", i).copy_(torch.as_tensor(g, dtype=dt))
+    if st.m is not None:
+        st.view("m", i).copy_(torch.as_tensor(m, dtype=dt))
+    if st.v is not None:
+        st.view("v", i).copy_(torch.as_tensor(v, dtype=dt))
+
+
+def _get(st, which, i):
+    return st.view(which, i).cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["sgd", "sgdm", "adam", "adamw"])
+def test_fp64_bitexact_vs_reference_golden(golden, name):
+    blk = golden["blocks"][name]
+    kind = NAMES[name]
+    h = OptimizerHyper(**{k: v for k, v in blk["hyper"].items()})
+    x0, g, m0, v0 = ([F(s) for s in blk[k]] for k in ("x0", "g", "m0", "v0"))
+    n = len(x0)
+    st = DeviceState([n], dtype=torch.float64, kind=kind)
+    _load(st, 0, x0, np.zeros(n), m0, v0)
+    st.write_markers([(blk["t0"], 0)])
+    grad = torch.zeros(st.total, dtype=torch.float64, device="cuda")
+    grad[:n] = torch.tensor(g, dtype=torch.float64)
+    st.step(h, [0], grad=grad)
+    st.check_finite()
+    assert st.markers() == [(blk["t0"] + 1, 1)]
+    assert np.array_equal(_bits(_get(st, "x", 0)), _bits([F(s) for s in blk["step"]["x"]]))
+    assert np.array_equal(_get(st, "g", 0), np.array(g))  # block.g = grad (optim.cpp:349)
+    if kind != SGD:
+        assert np.array_equal(_bits(_get(st, "m", 0)), _bits([F(s) for s in blk["step"]["m"]]))
+    if kind in (ADAM, ADAMW):
+        assert np.array_equal(_bits(_get(st, "v", 0)), _bits([F(s) for s in blk["step"]["v"]]))
+    st.undo(h, [0])
+    st.check_finite()
+    assert st.markers() == [(blk["t0"], 0)]
+    assert np.array_equal(_bits(_get(st, "x", 0)), _bits([F(s) for s in blk["undo"]["x"]]))
+    if kind != SGD:
+        assert np.array_equal(_bits(_get(st, "m", 0)), _bits([F(s) for s in blk["undo"]["m"]]))
+    if kind in (ADAM, ADAMW):
+        assert np.array_equal(_bits(_get(st, "v", 0)), _bits([F(s) for s in blk["undo"]["v"]]))
+
+
+def _random_groups(rng, kind, sizes, dtype):
+    out = []
+    for n in sizes:
+        x = rng.uniform(-1, 1, n)
+        g = rng.uniform(-0.1, 0.1, n)
+        m = rng.uniform(-0.05, 0.05, n) if kind != SGD else np.zeros(n)
+        v = rng.uniform(0, 1e-3, n) if kind in (ADAM, ADAMW, AMSGRAD) else np.zeros(n)
+        out.append(tuple(a.astype(dtype) for a in (x, g, m, v)))
+    return out
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("kind", [SGD, SGDM, ADAM, ADAMW])
+def test_multigroup_bitexact_vs_restatement(restate: Restate, kind, dtype):
+    """Ragged groups (sizes not multiples of the vector width or chunk), each at
+    its own t (distinct scalar sets in one launch), stepped in update order and
+    then undone — compared bit for bit with the restatement."""
+    rng = np.random.default_rng(kind * 10 + (dtype == np.float64))
+    sizes = [1, 3, 7, 64, 100, 1023, 4097, 8191, 8193, 20000, 70001]
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    st = DeviceState(sizes, dtype=tdt, kind=kind)
+    data = _random_groups(rng, kind, sizes, dtype)
+    t0 = [int(rng.integers(0, 30)) for _ in sizes]
+    for i, (x, g, m, v) in enumerate(data):
+        _load(st, i, x, np.zeros_like(g), m, v)
+    st.write_markers([(t, 0) for t in t0])
+    grad = torch.zeros(st.total, dtype=tdt, device="cuda")
+    for i, (x, g, m, v) in enumerate(data):
+        grad[st.offsets[i]:st.offsets[i] + sizes[i]] = torch.as_tensor(g)
+    h = HYP[kind]
+    st.step(h, grad=grad)
+    st.check_finite()
+    assert st.markers() == [(t + 1, 1) for t in t0]
+    stepped = []
+    for i, (x, g, m, v) in enumerate(data):
+        rx, rm, rv, _ = restate.step(kind, h, t0[i], x, g, m, v, dtype=dtype)
+        assert np.array_equal(_bits(_get(st, "x", i)), _bits(rx)), (i, sizes[i])
+        if kind != SGD:
+            assert np.array_equal(_bits(_get(st, "m", i)), _bits(rm)), i
+        if kind in (ADAM, ADAMW):
+            assert np.array_equal(_bits(_get(st, "v", i)), _bits(rv)), i
+        stepped.append((rx, g, rm, rv))
+    st.undo(h)
+    st.check_finite()
+    assert st.markers() == [(t, 0) for t in t0]
+    for i, (rx, g, rm, rv) in enumerate(stepped):
+        ux, um, uv, _ = restate.undo(kind, h, t0[i] + 1, rx, g, rm, rv, dtype=dtype)
+        assert np.array_equal(_bits(_get(st, "x", i)), _bits(ux)), i
+        if kind != SGD:
+            assert np.array_equal(_bits(_get(st, "m", i)), _bits(um)), i
+        if kind in (ADAM, ADAMW):
+            assert np.array_equal(_bits(_get(st, "v", i)), _bits(uv)), i
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_amsgrad_step_bitexact(restate, dtype):
+    rng = np.random.default_rng(9)
+    sizes = [5, 4099]
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    st = DeviceState(sizes, dtype=tdt, kind=AMSGRAD)
+    h = OptimizerHyper(kind=AMSGRAD, lr=1e-3, weight_decay=0.01)
+    data = _random_groups(rng, AMSGRAD, sizes, dtype)
+    vmax0 = [rng.uniform(0, 1e-3, n).astype(dtype) for n in sizes]
+    for i, (x, g, m, v) in enumerate(data):
+        _load(st, i, x, g, m, v)
+        st.view("vmax", i).copy_(torch.as_tensor(vmax0[i]))
+    st.step(h)
+    for i, (x, g, m, v) in enumerate(data):
+        rx, rm, rv, rvm, _ = restate.step_amsgrad(h, 0, x, g, m, v, vmax0[i], dtype=dtype)
+        assert np.array_equal(_bits(_get(st, "x", i)), _bits(rx))
+        assert np.array_equal(_bits(_get(st, "vmax", i)), _bits(rvm))
+    with pytest.raises(RwError) as e:
+        st.undo(h)
+    assert e.value.name == "NotInvertible"
+
+
+def test_guards_match_reference_order():
+    st = DeviceState([10, 10], kind=ADAM)
+    h = HYP[ADAM]
+    with pytest.raises(RwError) as e:
+        st.undo(h, [0])
+    assert e.value.name == "NothingToUndo"
+    st.step(h, [1])
+    with pytest.raises(RwError) as e:
+        st.step(h, [0, 1])                       # group 1 already stepped
+    assert e.value.name == "AlreadyUpdated"
+    assert st.markers() == [(0, 0), (1, 1)]      # nothing launched for group 0
+    with pytest.raises(RwError) as e:
+        st.step(OptimizerHyper(kind=AMSGRAD, require_invertible=True), [0])
+    assert e.value.name == "NotInvertible"
+    with pytest.raises(RwError) as e:
+        st.undo(OptimizerHyper(kind=ADAM, beta1=0.0), [1])
+    assert e.value.name == "NonInvertibleHyper"
+    with pytest.raises(RwError) as e:
+        st.undo(OptimizerHyper(kind=ADAM, lr=0.1, lr_table=[(1, -1.0)]), [1])
+    assert e.value.name == "InvalidConfig"
+    st2 = DeviceState([4], kind=SGDM)
+    st2.step(OptimizerHyper(kind=SGDM, momentum=0.0), [0])
+    with pytest.raises(RwError) as e:
+        st2.undo(OptimizerHyper(kind=SGDM, momentum=0.0), [0])
+    assert e.value.name == "NonInvertibleHyper"
+    st3 = DeviceState([4], kind=SGD)
+    st3.step(OptimizerHyper(kind=SGD, lr=1.0, weight_decay=1.0), [0])
+    with pytest.raises(RwError) as e:
+        st3.undo(OptimizerHyper(kind=SGD, lr=1.0, weight_decay=1.0), [0])
+    assert e.value.name == "NonInvertibleHyper"
+
+
+def test_numerical_error_after_mutation():
+    st = DeviceState([100, 100], kind=ADAM)
+    st.g.fill_(0.01)
+    st.g[st.offsets[1] + 7] = float("inf")
+    st.step(HYP[ADAM])
+    with pytest.raises(RwError) as e:
+        st.check_finite()
+    assert e.value.name == "NumericalError"
+    # like the reference, the mutation happened and t/updated advanced
+    assert st.markers() == [(1, 1), (1, 1)]
+    assert not torch.isfinite(st.view("x", 1)).all()
+    st.check_finite()  # flag consumed
+
+
+def test_crash_injection_markers():
+    """MidUpdate(k): after k groups in update order (reverse
+    layer order) exactly those groups carry updated=1 and t+1."""
+    G = 12
+    st = DeviceState([3000 + 17 * i for i in range(G)], kind=SGDM)
+    seeded_fill_(st.x, 11)
+    h = HYP[SGDM]
+    for k in (0, 1, 5, G):
+        st.write_markers([(4, 0)] * G)
+        st.step(h, stop_after=k)
+        mk = st.markers()
+        order = st.update_order()
+        for pos, gi in enumerate(order):
+            assert mk[gi] == ((5, 1) if pos < k else (4, 0)), (k, gi)
+
+
+def test_seeded_fill_bit_identical_to_host(restate):
+    for dt, npdt in ((torch.float64, np.float64), (torch.float32, np.float32)):
+        out = torch.empty(100003, dtype=dt, device="cuda")
+        seeded_fill_(out, 2302)
+        host = restate.seeded_fill(100003, 2302, dtype=npdt)
+        assert np.array_equal(_bits(out.cpu().numpy()), _bits(host))
+    # counter offset = the same stream continued
+    out = torch.empty(1000, dtype=torch.float64, device="cuda")
+    seeded_fill_(out, 7, offset=500)
+    assert np.array_equal(out.cpu().numpy(), restate.seeded_fill(1500, 7)[500:])
+
+
+@pytest.mark.parametrize("count", [1, 2, 9, 70])
+def test_ordered_sum_bit_identical(restate, count):
+    rng = np.random.default_rng(count)
+    for dt, npdt in ((torch.float64, np.float64), (torch.float32, np.float32)):
+        arrs = [(rng.standard_normal(5001) * 10.0 ** rng.integers(-4, 4)).astype(npdt)
+                for _ in range(count)]
+        out = ordered_sum([torch.as_tensor(a, device="cuda") for a in arrs])
+        assert np.array_equal(_bits(out.cpu().numpy()), _bits(restate.ordered_sum(arrs, dtype=npdt)))
+
+
+def test_large_state_roundtrip_sampled(restate):
+    """At a large size: step + undo in one launch each over 64 groups; check
+    bitwise against the restatement on a random sample of elements (the ops are
+    elementwise, so sampling is exact) and the SPEC:132 round-trip property."""
+    sizes = [1_000_003 + 4099 * i for i in range(64)]
+    st = DeviceState(sizes, kind=ADAM)
+    seeded_fill_(st.x, 1)
+    seeded_fill_(st.m, 2)
+    st.m.mul_(0.01)
+    seeded_fill_(st.v, 3)
+    st.v.abs_().mul_(1e-4)
+    grad = torch.empty_like(st.x)
+    seeded_fill_(grad, 4)
+    x0, m0, v0 = st.x.clone(), st.m.clone(), st.v.clone()
+    st.write_markers([(7, 0)] * len(sizes))
+    h = HYP[ADAM]
+    st.step(h, grad=grad)
+    xs = st.x.clone()
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    gi = torch.randint(0, len(sizes), (200_000,), device="cuda", generator=gen)
+    offs = torch.tensor(st.offsets, device="cuda")[gi]
+    lens = torch.tensor(sizes, device="cuda")[gi]
+    idx = offs + (torch.rand(200_000, device="cuda", generator=gen) * lens).long().clamp_max(lens - 1)
+    rx, rm, rv, _ = restate.step(ADAM, h, 7, x0[idx].cpu().numpy(), grad[idx].cpu().numpy(),
+                                 m0[idx].cpu().numpy(), v0[idx].cpu().numpy(), dtype=np.float32)
+    assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(rx))
+    assert np.array_equal(_bits(st.v[idx].cpu().numpy()), _bits(rv))
+    st.undo(h)
+    st.check_finite()
+    ux, um, uv, _ = restate.undo(ADAM, h, 8, rx, grad[idx].cpu().numpy(), rm, rv, dtype=np.float32)
+    assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(ux))
+    assert np.array_equal(_bits(st.m[idx].cpu().numpy()), _bits(um))
+    # fp32 round trip: x within 1 ulp of max(|x_t|, |x_t+1|)
+    sp = torch.maximum(x0.abs(), xs.abs())
+    assert ((st.x - x0).abs() <= 2 * torch.finfo(torch.float32).eps * sp + 1e-30).all()
