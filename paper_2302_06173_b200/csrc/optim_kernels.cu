@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     T* vs = slot(st, SV);
     T* ws = slot(st, SW);
     T zero_m = T(0), zero_v = T(0), zero_w = T(0);
-    for (uint32_t e = tid * EV; e < nbulk; e += kThreads * EV) {
+    auto body = [&](uint32_t e) {
       V xr = *reinterpret_cast<const V*>(xs + e);
       V gr = *reinterpret_cast<const V*>(gs + e);
       V mr, vr, wr;
@@ -401,6 +401,13 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
       if constexpr (U::m) *reinterpret_cast<V*>(ms + e) = mr;
       if constexpr (U::v) *reinterpret_cast<V*>(vs + e) = vr;
       if constexpr (U::vmax) *reinterpret_cast<V*>(ws + e) = wr;
+    };
+    if (nbulk == TILE) {  // full tile: compile-time trip count, unrolled for ILP
+      constexpr uint32_t kIters = TILE / (kThreads * EV);
+#pragma unroll
+      for (uint32_t k = 0; k < kIters; ++k) body(tid * EV + k * kThreads * EV);
+    } else {
+      for (uint32_t e = tid * EV; e < nbulk; e += kThreads * EV) body(e);
     }
     // unaligned head/tail elements straight from global memory
     if (tid < nhead + ntail) {

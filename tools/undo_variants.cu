@@ -257,17 +257,19 @@ __global__ void __launch_bounds__(T, 1) undo_tma(float* __restrict__ x, const fl
     bulk_load(b + 2 * TILE, m + off, TILE * 4, &full[st]);
     bulk_load(b + 3 * TILE, v + off, TILE * 4, &full[st]);
   };
-  uint64_t first = blockIdx.x;
-  const uint64_t step = gridDim.x;
+  const uint64_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  uint64_t first = DEFER == 2 ? blockIdx.x * per : blockIdx.x;
+  const uint64_t step = DEFER == 2 ? 1 : gridDim.x;
+  const uint64_t tend = DEFER == 2 ? (first + per < ntiles ? first + per : ntiles) : ntiles;
   if (tid == 0) {
     for (int k = 0; k < S; ++k) {
       uint64_t t = first + k * step;
-      if (t < ntiles) issue(t, k);
+      if (t < tend) issue(t, k);
     }
   }
   bool bad = false;
   int it = 0;
-  for (uint64_t t = first; t < ntiles; t += step, ++it) {
+  for (uint64_t t = first; t < tend; t += step, ++it) {
     const int st = it % S;
     const uint32_t par = (it / S) & 1;
     mbar_wait(&full[st], par);
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(T, 1) undo_tma(float* __restrict__ x, const fl
           bulk_wait<1>();  // previous tile's stores complete
           const int ps = (it - 1) % S;
           uint64_t nt = t - step + uint64_t(S) * step;
-          if (nt < ntiles) issue(nt, ps);
+          if (nt < tend) issue(nt, ps);
         }
       } else {
         uint64_t nt = t + uint64_t(S) * step;
@@ -483,6 +485,11 @@ int main(int argc, char** argv) {
   };
   tma("TMA t2048 S3 T256 imm", undo_tma<0, 2048, 3, 256, 0>, 2048, 3, 256);
   tma("TMA t2048 S3 T256 defer", undo_tma<0, 2048, 3, 256, 1>, 2048, 3, 256);
+  tma("TMA t2048 S3 T256 defer CONTIG", undo_tma<0, 2048, 3, 256, 2>, 2048, 3, 256);
+  tma("TRIV-TMA t2048 S3 T256 defer", undo_tma<2, 2048, 3, 256, 1>, 2048, 3, 256);
+  tma("TRIV-TMA t2048 S3 T256 CONTIG", undo_tma<2, 2048, 3, 256, 2>, 2048, 3, 256);
+  tma("TMA t2048 S4 T256 defer (1/SM?)", undo_tma<0, 2048, 4, 256, 1>, 2048, 4, 256);
+  tma("TMA t1024 S6 T256 defer", undo_tma<0, 1024, 6, 256, 1>, 1024, 6, 256);
   tma("TMA t2048 S3 T384 imm", undo_tma<0, 2048, 3, 384, 0>, 2048, 3, 384);
   tma("TMA t2048 S3 T512 imm", undo_tma<0, 2048, 3, 512, 0>, 2048, 3, 512);
   tma("TMA t2048 S3 T512 defer", undo_tma<0, 2048, 3, 512, 1>, 2048, 3, 512);
