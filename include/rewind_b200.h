@@ -153,6 +153,19 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* group_ids,
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
                       void* stream);
 
+/* ---- host-buffer entry points: ONE reference ParamBlock held in host memory ----
+ * Exactly optimizer_step / optimizer_undo (optim.cpp:338-385) on a block whose
+ * x, g, m, v (and AMSGrad vmax) live in host memory: the library stages them
+ * through device memory it owns (per calling thread), runs the fused kernel,
+ * copies the results back and reports NumericalError like the reference
+ * (after mutation).  dtype RW_F64 reproduces the reference bit for bit.
+ * t/updated are the block's marker, read and written.  vmax may be NULL
+ * except for AMSGrad; m/v may be NULL when the kind does not use them. */
+int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* vmax, uint64_t n,
+                       uint64_t* t, uint32_t* updated, const void* grad, const rw_hyper* h);
+int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n,
+                       uint64_t* t, uint32_t* updated, const rw_hyper* h);
+
 /* ---- consistency resolver (no reference source) ---- */
 enum { RW_ACT_NONE = 0, RW_ACT_UNDO = 1, RW_ACT_REDO = 2 };
 enum { RW_POLICY_UNDO = 0 /* paper: always roll back to min */, RW_POLICY_MIN_COST = 1 };

@@ -547,3 +547,133 @@ int rw_ordered_sum(int32_t dtype, const void* const* tensors, uint32_t count, ui
 }
 
 }  // extern "C"
+
+// ---------------- host-buffer ParamBlock entry points ----------------
+namespace {
+
+// Per-thread staging area: device copies of one block + a one-group rw_state.
+struct HostStage {
+  int dtype = -1;
+  uint64_t n = 0;
+  int device = -1;
+  void* d[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // x g m v vmax
+  rw_state* st = nullptr;
+  cudaStream_t stream = nullptr;
+  void release() {
+    if (st) rw_state_destroy(st);
+    st = nullptr;
+    for (auto& p : d) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    n = 0;
+  }
+  ~HostStage() {
+    release();
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+thread_local HostStage g_stage;
+
+int stage_prepare(int dtype, uint64_t n) {
+  if (rw_device_count() == 0) return fail(RW_CUDA_ERROR, "no CUDA device visible: the B200 path has no CPU fallback");
+  int dev = 0;
+  RW_CUDA(cudaGetDevice(&dev));
+  HostStage& S = g_stage;
+  if (S.st && S.dtype == dtype && S.n == n && S.device == dev) return RW_OK;
+  S.release();
+  S.dtype = dtype;
+  S.n = n;
+  S.device = dev;
+  if (!S.stream) RW_CUDA(cudaStreamCreateWithFlags(&S.stream, cudaStreamNonBlocking));
+  const size_t bytes = n * elem_size(dtype);
+  for (auto& p : S.d) RW_CUDA(cudaMalloc(&p, bytes));
+  rw_group gr{0, n, 0, 0, 0};
+  return rw_state_create(&S.st, dtype, S.d[0], S.d[1], S.d[2], S.d[3], S.d[4], n, &gr, 1, dev);
+}
+
+int block_guards_step(const rw_hyper* h, uint64_t t, uint32_t updated, double* eta) {
+  if (updated) return fail(RW_ALREADY_UPDATED, "AlreadyUpdated: block already stepped this iteration");
+  if (h->require_invertible && rw_invertibility_check(h->kind) == RW_NOT_INVERTIBLE_KIND)
+    return fail(RW_NOT_INVERTIBLE, "NotInvertible: %s cannot be undone", kind_name(h->kind));
+  return lr_at(h, t + 1, eta);
+}
+
+}  // namespace
+
+extern "C" {
+
+// optimizer_step on a host ParamBlock (optim.cpp:338-364)
+int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* vmax, uint64_t n,
+                       uint64_t* t, uint32_t* updated, const void* grad, const rw_hyper* h) {
+  if (!x || !g || !t || !updated || !h || !grad) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "bad dtype");
+  if (n == 0) return fail(RW_INVALID_SHAPE, "InvalidShape: zero extent");
+  const size_t bytes = n * elem_size(dtype);
+  double eta = 0;
+  int st = block_guards_step(h, *t, *updated, &eta);
+  if (st) {
+    if (st == RW_INVALID_CONFIG) std::memcpy(g, grad, bytes);  // :349 runs before :350 raises
+    return st;
+  }
+  const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_AMSGRAD;
+  if ((um && !m) || (uv && !v) || (h->kind == RW_AMSGRAD && !vmax))
+    return fail(RW_INVALID_ARGUMENT, "%s needs its m/v/vmax buffers", kind_name(h->kind));
+  if (h->kind == RW_LAMB) return fail(RW_INVALID_ARGUMENT, "lamb is not on the B200 path yet (SURVEY §8f rank 2)");
+  st = stage_prepare(dtype, n);
+  if (st) return st;
+  HostStage& S = g_stage;
+  void* hs[5] = {x, const_cast<void*>(grad), m, v, vmax};
+  const bool use[5] = {true, true, um, uv, h->kind == RW_AMSGRAD};
+  for (int i = 0; i < 5; ++i)
+    if (use[i]) RW_CUDA(cudaMemcpyAsync(S.d[i], hs[i], bytes, cudaMemcpyHostToDevice, S.stream));
+  rw_group gr{0, n, *t, 0, 0};
+  st = rw_state_write_groups(S.st, &gr, S.stream);
+  if (st) return st;
+  const uint32_t id = 0;
+  st = rw_optimizer_step(S.st, h, &id, 1, nullptr, UINT32_MAX, S.stream);
+  if (st) return st;
+  void* outs[5] = {x, g, m, v, vmax};
+  for (int i = 0; i < 5; ++i)
+    if (use[i]) RW_CUDA(cudaMemcpyAsync(outs[i], S.d[i], bytes, cudaMemcpyDeviceToHost, S.stream));
+  *t += 1;  // optim.cpp:359-360
+  *updated = 1;
+  return rw_state_check(S.st, S.stream);  // :361-363, after mutation
+}
+
+// optimizer_undo on a host ParamBlock (optim.cpp:366-385)
+int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
+                       uint32_t* updated, const rw_hyper* h) {
+  if (!x || !g || !t || !updated || !h) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "bad dtype");
+  if (n == 0) return fail(RW_INVALID_SHAPE, "InvalidShape: zero extent");
+  // the guards (NothingToUndo, AMSGrad, lr_at, per-kind hyper) run inside
+  // rw_optimizer_undo before any launch; check the flag first so a refused
+  // call never touches the device.
+  if (!*updated) return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: block has no pending update");
+  if (h->kind == RW_AMSGRAD) return fail(RW_NOT_INVERTIBLE, "NotInvertible: amsgrad element-wise max has no inverse");
+  const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW;
+  if ((um && !m) || (uv && !v)) return fail(RW_INVALID_ARGUMENT, "%s needs its m/v buffers", kind_name(h->kind));
+  int st = stage_prepare(dtype, n);
+  if (st) return st;
+  HostStage& S = g_stage;
+  const size_t bytes = n * elem_size(dtype);
+  rw_group gr{0, n, *t, 1, 0};
+  st = rw_state_write_groups(S.st, &gr, S.stream);
+  if (st) return st;
+  void* hs[4] = {x, g, m, v};
+  const bool use[4] = {true, true, um, uv};
+  const uint32_t id = 0;
+  for (int i = 0; i < 4; ++i)
+    if (use[i]) RW_CUDA(cudaMemcpyAsync(S.d[i], hs[i], bytes, cudaMemcpyHostToDevice, S.stream));
+  st = rw_optimizer_undo(S.st, h, &id, 1, S.stream);
+  if (st) return st;
+  const bool out[4] = {true, false, um, uv};
+  for (int i = 0; i < 4; ++i)
+    if (out[i]) RW_CUDA(cudaMemcpyAsync(hs[i], S.d[i], bytes, cudaMemcpyDeviceToHost, S.stream));
+  *t -= 1;  // optim.cpp:380-381
+  *updated = 0;
+  return rw_state_check(S.st, S.stream);  // :382-384, after mutation
+}
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+"""Host logic of the N>1 recovery path (resolver all-reduces + replica
+broadcast) with world-size-2 gloo on CPU.  The orchestration code is the same
+one bench.py runs over NCCL on the B200 box; only the tensors are host
+tensors here (HostState mimics the DeviceState surface it touches)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2302_06173_b200 import ADAM, AMSGRAD, OptimizerHyper
+from paper_2302_06173_b200.recovery import recover_replication, resolve
+
+
+class HostState:
+    def __init__(self, sizes, seed=None):
+        n = sum(sizes)
+        self.device = torch.device("cpu")
+        g = torch.Generator().manual_seed(seed or 0)
+        mk = (lambda: torch.randn(n, generator=g)) if seed is not None else (lambda: torch.zeros(n))
+        self.x, self.g, self.m, self.v = mk(), mk(), mk(), mk()
+        self._mk = [(0, 0)] * len(sizes)
+
+    def markers(self, stream=None):
+        return list(self._mk)
+
+    def write_markers(self, mk, stream=None):
+        self._mk = [tuple(p) for p in mk]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, scenario, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out = scenario(rank)
+        q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(scenario, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, scenario, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def scen_survivor_and_replacement(rank):
+    h = OptimizerHyper(kind=ADAM)
+    if rank == 0:  # survivor crashed mid-update: layers 1,2 updated (reverse order)
+        mk = [(10, 0), (11, 1), (11, 1)]
+        plan = resolve(mk, h, lens=[5, 5, 5])
+        st = HostState([5, 5, 5], seed=3)
+        st.write_markers([(10, 0), (10, 0), (10, 0)])  # after apply_resolution
+    else:          # replacement: no state, joins the consensus with nothing
+        plan = resolve([], h)
+        st = HostState([5, 5, 5])
+    nbytes = recover_replication(st, src=0)
+    return dict(strategy=plan.strategy, target=plan.target, undo=plan.undo_ids,
+                x=st.x.clone(), m=st.m.clone(), v=st.v.clone(), mk=st.markers(), nbytes=nbytes)
+
+
+def test_replication_recovery_world2():
+    res = _run(scen_survivor_and_replacement)
+    a, b = res[0], res[1]
+    assert a["strategy"] == b["strategy"] == "Undo"
+    assert a["target"] == b["target"] == 10
+    assert a["undo"] == [1, 2] and b["undo"] == []
+    for k in ("x", "m", "v"):  # bit-exact copy semantics
+        assert torch.equal(a[k].view(torch.int32), b[k].view(torch.int32))
+    assert b["mk"] == [(10, 0)] * 3
+    assert a["nbytes"] == 3 * 15 * 4
+
+
+def scen_two_survivors_redo(rank):
+    h = OptimizerHyper(kind=ADAM)
+    # rank 0 updated 2 of 3 groups, rank 1 updated 1 of 3; gradients landed everywhere
+    mk = [[(5, 0), (6, 1), (6, 1)], [(5, 0), (5, 0), (6, 1)]][rank]
+    plan_min = resolve(mk, h, lens=[100, 100, 100], grad_ready=[True] * 3, policy="min_cost")
+    plan_undo = resolve(mk, h, lens=[100, 100, 100], grad_ready=[True] * 3, policy="undo")
+    plan_blocked = resolve(mk, h, lens=[100, 100, 100], grad_ready=[False] * 3, policy="min_cost")
+    plan_ams = resolve(mk, OptimizerHyper(kind=AMSGRAD), lens=[100, 100, 100],
+                       grad_ready=[True] * 3)
+    return dict(min=(plan_min.strategy, plan_min.target, plan_min.actions),
+                undo=(plan_undo.strategy, plan_undo.target, plan_undo.actions),
+                blocked=plan_blocked.strategy, ams=(plan_ams.strategy, plan_ams.target))
+
+
+def test_resolver_two_survivors_world2():
+    res = _run(scen_two_survivors_redo)
+    # max over ranks: undo cost = 200 elems (rank 0), redo cost = 200 (rank 1) -> tie -> undo
+    assert res[0]["min"][0] == "Undo" and res[0]["min"][1] == 5
+    assert res[0]["undo"] == ("Undo", 5, [0, 1, 1]) and res[1]["undo"] == ("Undo", 5, [0, 0, 1])
+    assert res[0]["blocked"] == "Undo"
+    # AMSGrad cannot undo but every lagging group holds its gradient -> redo to 6
+    assert res[0]["ams"] == ("Redo", 6) and res[1]["ams"] == ("Redo", 6)
