@@ -110,10 +110,13 @@ class DeviceState:
     """
 
     def __init__(self, sizes: Sequence[int], dtype: torch.dtype = torch.float32,
-                 device: int | torch.device = 0, kind: int = ADAM, with_vmax: bool = False,
+                 device: int | torch.device | None = None, kind: int = ADAM,
+                 with_vmax: bool = False,
                  align: int = ALIGN_ELEMS):
         if not torch.cuda.is_available():
             raise RwError(_lib.RW_CUDA_ERROR, "no CUDA device: the B200 path has no CPU fallback")
+        if device is None:
+            device = torch.cuda.current_device()
         dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.device = dev
         self.dtype = dtype
