@@ -1,0 +1,384 @@
+// Blackwell (sm_100a) bf16 GEMM on the 5th-gen tensor cores, hand-written:
+//   TMA (cp.async.bulk.tensor, 128B swizzle) -> smem ring (kStages)
+//   -> one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//      (M=128, N=BN, K=16 per instruction) into a TMEM fp32 accumulator
+//   -> 4 epilogue warps: tcgen05.ld -> fused epilogue -> global.
+// Persistent: one CTA per SM walks output tiles; two TMEM accumulator stages
+// let the epilogue of tile i overlap the MMAs of tile i+1.
+//
+// C[M,N] = A[M,K] . B[N,K]^T  (UMMA convention), where each operand is
+// either K-major (K contiguous) or MN-major (M resp. N contiguous) in global
+// memory.  This covers the three replay GEMMs of an affine layer
+// (model.cpp:59-73, 121-147) without transposes:
+//   forward  Y[R,N]  = X[R,K] . W[K,N]     A=X  K-major, B=W  MN-major
+//   dgrad    dX[R,K] = dZ[R,N] . W[K,N]^T  A=dZ K-major, B=W  K-major
+//   wgrad    dW[K,N] = X[R,K]^T . dZ[R,N]  A=X  MN-major, B=dZ MN-major
+//
+// Determinism: fixed tiling, no split-K, no atomics: identical inputs give
+// identical bits (the GPU "ghost run" contract of SURVEY §7 hard part 5).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace rwb {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;     // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kThreads = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-7 epilogue
+constexpr int kEpiWarp0 = 4;
+
+enum Major : int { K_MAJOR = 0, MN_MAJOR = 1 };
+
+enum Epi : int {
+  EPI_BF16 = 0,           // out_bf16 = acc
+  EPI_BIAS_TANH_BF16 = 1, // out_bf16 = tanh(acc + bias[n])            (forward)
+  EPI_DTANH_BF16 = 2,     // out_bf16 = acc * (1 - y[m,n]^2)           (dgrad -> next dz)
+  EPI_F32 = 3,            // out_f32  = acc                             (wgrad, first mb)
+  EPI_F32_ACC = 4,        // out_f32  = out_f32 + acc                   (wgrad, ordered mb sum)
+};
+
+struct EpiArgs {
+  void* out;             // bf16 or f32 [M, N] row-major, leading dim ldo (elements)
+  int64_t ldo;
+  const float* bias;     // [N] (EPI_BIAS_TANH_BF16)
+  const __nv_bfloat16* y;  // [M, N] row-major, ld ldy (EPI_DTANH_BF16)
+  int64_t ldy;
+};
+
+// ---------------------------------------------------------------- PTX
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// Waits on an mbarrier phase.  A pipeline bug must not hang the GPU: after
+// ~2^34 cycles (several seconds) the kernel traps instead.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  const long long t0 = clock64();
+  while (true) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns: thread i gets row (lane base + i)
+__device__ __forceinline__ void tmem_ld_32cols(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor (SM100 "version 1"), SWIZZLE_128B.
+//   K-major : rows of 128 B (64 bf16 of K); 8-row groups 1024 B apart (SBO).
+//   MN-major: rows of 128 B (64 bf16 of M/N) per K index; 8 K-rows = 1024 B
+//             (SBO); successive 64-wide M/N chunks LBO bytes apart.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;  // version = 1 (Blackwell)
+  d |= uint64_t(2) << 61;  // layout = SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, dense
+__host__ __device__ constexpr uint32_t make_idesc(int m, int n, int a_major, int b_major) {
+  return (1u << 4)                      // c_format F32
+         | (1u << 7)                    // a_format BF16
+         | (1u << 10)                   // b_format BF16
+         | (uint32_t(a_major) << 15)    // a major
+         | (uint32_t(b_major) << 16)    // b major
+         | (uint32_t(n >> 3) << 17)     // N / 8
+         | (uint32_t(m >> 4) << 24);    // M / 16
+}
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB
+  static constexpr uint32_t kBBytes = BN * BK * 2;   // 32 KB (BN=256)
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = 2 * BN;      // two accumulator stages
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024;  // + alignment slack
+};
+
+// smem layout inside one operand buffer for MN-major tiles: TMA boxes of
+// {64 (MN), 64 (K)} stacked along MN every 64*128 B = 8 KB  => LBO = 8192.
+constexpr uint32_t kMnChunkBytes = 64 * 128;
+
+template <int BN, int AMAJ, int BMAJ, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     int M, int N, int K, EpiArgs ep) {
+  using C = Cfg<BN>;
+  constexpr int S = C::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-byte aligned base for the swizzled tiles
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles_m = (M + BM - 1) / BM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tma_a);
+    prefetch_tmap(&tma_b);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 4);  // one arrive per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {  // TMEM allocation (whole warp), address published via smem
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int tm = tile % tiles_m, tn = tile / tiles_m;  // M-fastest: B tile reused via L2
+        const int m0 = tm * BM, n0 = tn * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          mbar_expect_tx(&full_bar[stage], C::kStageBytes);
+          const int k0 = kb * BK;
+          if constexpr (AMAJ == K_MAJOR) {
+            tma_load_2d(sa, &tma_a, &full_bar[stage], k0, m0);  // box {64 K, 128 M}
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c)                    // boxes {64 M, 64 K}
+              tma_load_2d(sa + c * kMnChunkBytes, &tma_a, &full_bar[stage], m0 + c * 64, k0);
+          }
+          if constexpr (BMAJ == K_MAJOR) {
+            tma_load_2d(sb, &tma_b, &full_bar[stage], k0, n0);  // box {64 K, BN N}
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c)
+              tma_load_2d(sb + c * kMnChunkBytes, &tma_b, &full_bar[stage], n0 + c * 64, k0);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    constexpr uint32_t idesc = make_idesc(BM, BN, AMAJ, BMAJ);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      mbar_wait(&tempty_bar[acc], acc_phase ^ 1);  // epilogue drained this accumulator
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16-element K step inside the 128 B swizzle row
+            // MN-major: +2 K-row groups (2 x 1024 B) per 16-element K step
+            const uint64_t ad = AMAJ == K_MAJOR ? make_desc(sa + k * 32, 16, 1024)
+                                                : make_desc(sa + k * 2048, kMnChunkBytes, 1024);
+            const uint64_t bd = BMAJ == K_MAJOR ? make_desc(sb + k * 32, 16, 1024)
+                                                : make_desc(sb + k * 2048, kMnChunkBytes, 1024);
+            tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty_bar[stage]);  // frees the smem stage when these MMAs finish
+        }
+        __syncwarp();
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) tc_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ===================== epilogue (warps 4..7 -> TMEM lanes 0..127) =====================
+    const int ew = warp - kEpiWarp0;  // == warp % 4: TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      const int m0 = tm * BM, n0 = tn * BN;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld_32cols(tbase + uint32_t(c0), v);
+        const int col0 = n0 + c0;
+        if (row < M) {
+          if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
+            float* o = static_cast<float*>(ep.out) + int64_t(row) * ep.ldo + col0;
+            if (col0 + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                float4 w = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                if constexpr (EPI == EPI_F32_ACC) {
+                  const float4 p = *reinterpret_cast<const float4*>(o + j);
+                  w.x = __fadd_rn(p.x, w.x);
+                  w.y = __fadd_rn(p.y, w.y);
+                  w.z = __fadd_rn(p.z, w.z);
+                  w.w = __fadd_rn(p.w, w.w);
+                }
+                *reinterpret_cast<float4*>(o + j) = w;
+              }
+            } else {
+              for (int j = 0; j < 32 && col0 + j < N; ++j)
+                o[j] = EPI == EPI_F32_ACC ? __fadd_rn(o[j], v[j]) : v[j];
+            }
+          } else {
+            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + int64_t(row) * ep.ldo + col0;
+            float w[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float a = v[j];
+              if constexpr (EPI == EPI_BIAS_TANH_BF16) {
+                const float b = (col0 + j < N) ? __ldg(ep.bias + col0 + j) : 0.f;
+                a = tanhf(__fadd_rn(a, b));
+              } else if constexpr (EPI == EPI_DTANH_BF16) {
+                float yv = 0.f;
+                if (col0 + j < N) yv = __bfloat162float(ep.y[int64_t(row) * ep.ldy + col0 + j]);
+                a = __fmul_rn(a, __fsub_rn(1.f, __fmul_rn(yv, yv)));
+              }
+              w[j] = a;
+            }
+            if (col0 + 32 <= N) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                uint4 pk;
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(w[j], w[j + 1]);
+                __nv_bfloat162 h1 = __floats2bfloat162_rn(w[j + 2], w[j + 3]);
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(w[j + 4], w[j + 5]);
+                __nv_bfloat162 h3 = __floats2bfloat162_rn(w[j + 6], w[j + 7]);
+                pk.x = *reinterpret_cast<uint32_t*>(&h0);
+                pk.y = *reinterpret_cast<uint32_t*>(&h1);
+                pk.z = *reinterpret_cast<uint32_t*>(&h2);
+                pk.w = *reinterpret_cast<uint32_t*>(&h3);
+                *reinterpret_cast<uint4*>(o + j) = pk;
+              }
+            } else {
+              for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(w[j]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(C::kTmemCols));
+  }
+}
+
+}  // namespace gemm
+}  // namespace rwb

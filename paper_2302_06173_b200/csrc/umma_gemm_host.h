@@ -1,0 +1,76 @@
+// Host helpers for umma_gemm.cuh: TMA tensor maps (driver entry point fetched
+// through the runtime, so nothing links libcuda directly) and the launcher.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "umma_gemm.cuh"
+
+namespace rwb {
+namespace gemm {
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                   CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 row-major matrix [rows, cols] (cols contiguous, row pitch ld
+// elements), box {64 cols, box_rows rows}, 128-byte swizzle, OOB -> zeros.
+inline int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                    uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return static_cast<int>(cudaErrorNotSupported);
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
+}
+
+// C[M,N] (+)= A . B^T with A given as [M,K] (K_MAJOR) or [K,M] (MN_MAJOR) and
+// B as [N,K] (K_MAJOR) or [K,N] (MN_MAJOR); lda/ldb = row pitch in elements.
+template <int BN, int AMAJ, int BMAJ, int EPI>
+int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
+           cudaStream_t stream, int max_ctas = 0) {
+  CUtensorMap ma, mb;
+  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM) : make_map(&ma, A, K, M, lda, 64);
+  if (e) return e;
+  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN) : make_map(&mb, B, K, N, ldb, 64);
+  if (e) return e;
+  auto kern = umma_gemm_kernel<BN, AMAJ, BMAJ, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(Cfg<BN>::kSmem));
+    if (ce != cudaSuccess) return static_cast<int>(ce);
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  int grid = tiles < sms ? tiles : sms;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+  kern<<<grid, kThreads, Cfg<BN>::kSmem, stream>>>(ma, mb, M, N, K, ep);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace gemm
+}  // namespace rwb
