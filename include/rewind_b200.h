@@ -205,6 +205,45 @@ uint64_t rw_derive_seed(uint64_t base, const uint64_t* parts, uint32_t n);
 int rw_ordered_sum(int32_t dtype, const void* const* tensors, uint32_t count, uint64_t n,
                    void* out, void* stream);
 
+/* ---- replay compute: one pipeline stage (model.hpp:16-70) ----
+ * A stage is num_layers affine+tanh layers; dims[l] -> dims[l+1].  Weights are
+ * bf16 [dims[l], dims[l+1]] row-major (the reference W layout, model.cpp:67,
+ * `W[k*out+c]`), usually the bf16 shadow of the fp32 master x of the stage's
+ * rw_state; biases are the fp32 master values.  Activations are bf16 [rows, dim]
+ * row-major.  GEMMs run on the tcgen05 tensor cores (fp32 accumulation). */
+enum { RW_BF16 = 2 };
+typedef struct rw_stage_desc {
+  int32_t num_layers;
+  int32_t _pad;
+  const int64_t* dims;      /* num_layers + 1 */
+  const void* const* w;     /* num_layers bf16 device pointers */
+  const float* const* b;    /* num_layers fp32 device pointers */
+} rw_stage_desc;
+
+/* forward_stage (model.cpp:77-92): acts[0] = the stage input (caller-filled);
+ * acts[l+1] = tanh(acts[l] . W_l + b_l) is written (the activation cache the
+ * backward consumes). */
+int rw_stage_forward(const rw_stage_desc* st, int64_t rows, void* const* acts, void* stream);
+
+/* backward_stage (model.cpp:94-156) + accumulate_grads (:158-172):
+ * grad_in = dL/d(acts[L]) [rows, dims[L]] bf16; grad_out = dL/d(acts[0])
+ * [rows, dims[0]] bf16 (NULL to skip the first layer's dgrad);
+ * dw[l] fp32 [dims[l], dims[l+1]], db[l] fp32 [dims[l+1]]: overwritten when
+ * accumulate == 0 (first micro-batch) else added (ascending micro-batch order,
+ * ordered_sum semantics).  scratch: 2 bf16 buffers of rows*max(dims) elements
+ * plus one fp32 buffer of 64*max(dims) elements. */
+int rw_stage_backward(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
+                      void* grad_out, float* const* dw, float* const* db, int32_t accumulate,
+                      void* scratch_dz0, void* scratch_dz1, float* scratch_f32, void* stream);
+
+/* mse_loss (model.cpp:174-188): grad = 2/(n*micro_batches) * (pred - target)
+ * (bf16 out); *loss (device double, may be NULL) = mean squared error.
+ * scratch: 256 doubles. */
+int rw_mse_grad(const void* pred_bf16, const float* target, uint64_t n, uint64_t micro_batches,
+                void* grad_bf16, double* loss, double* scratch, void* stream);
+/* fp32 -> bf16 (weight shadows after an optimizer step) */
+int rw_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream);
+
 /* ---- selective-logging policy (planner.cpp missing) ---- */
 /* bubble_ratio(p, m), schedule.cpp:86-93 */
 int rw_bubble_ratio(int32_t p, int32_t m, int64_t* num, int64_t* den);

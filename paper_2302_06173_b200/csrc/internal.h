@@ -62,4 +62,18 @@ int launch_ordered_sum(int dtype, const void* const* tensors, uint32_t count, ui
                        void* stream);
 int launch_clear_updated(rw_group* groups, const uint32_t* ids, uint32_t n, void* stream);
 
+// replay_kernels.cu (all return cudaError_t as int)
+int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, const void* w, const float* b,
+                         void* y, void* stream);
+int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
+                       const void* y_prev, void* dst, void* stream);
+int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
+                       int accumulate, void* stream);
+int replay_dtanh_first(const void* g, const void* y, void* dz, uint64_t n, void* stream);
+int replay_colsum(const void* dz, int64_t rows, int64_t cols, float* db, float* scratch, int accumulate,
+                  void* stream);
+int replay_cast_bf16(const float* in, void* out, uint64_t n, void* stream);
+int replay_mse_grad(const void* pred, const float* target, uint64_t n, uint64_t micro_batches, void* grad,
+                    double* loss, double* scratch, void* stream);
+
 }  // namespace rwb

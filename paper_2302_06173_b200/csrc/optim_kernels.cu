@@ -26,6 +26,7 @@
 //   6.0-6.3 TB/s for register-staged 128/256-bit LDG/STG variants.
 // Ragged tile ends (groups are 256 B aligned by the layout builder, but the C
 // ABI accepts any offset) are handled element-wise from global memory.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -536,7 +537,8 @@ __global__ void seeded_fill_kernel(T* __restrict__ out, uint64_t n, uint64_t see
     // unit = (r >> 11) * 2^-53 exactly; (unit * 2 - 1) exact; * 0.1 one rounding
     const double unit = __dmul_rn(static_cast<double>(r >> 11), 0x1.0p-53);
     const double val = __dmul_rn(__dsub_rn(__dmul_rn(unit, 2.0), 1.0), 0.1);
-    out[i] = static_cast<T>(val);
+    if constexpr (sizeof(T) == 2) out[i] = __double2bfloat16(val);  // one rounding
+    else out[i] = static_cast<T>(val);
   }
 }
 
@@ -599,6 +601,8 @@ int launch_seeded_fill(int dtype, void* out, uint64_t n, uint64_t seed, uint64_t
   const int grid = grid_for(n, 256);
   if (dtype == RW_F64)
     seeded_fill_kernel<double><<<grid, 256, 0, st>>>(static_cast<double*>(out), n, sm, offset);
+  else if (dtype == RW_BF16)
+    seeded_fill_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(out), n, sm, offset);
   else
     seeded_fill_kernel<float><<<grid, 256, 0, st>>>(static_cast<float*>(out), n, sm, offset);
   return static_cast<int>(cudaGetLastError());

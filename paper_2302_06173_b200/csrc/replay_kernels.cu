@@ -1,0 +1,171 @@
+// Replay compute of one pipeline stage on the B200 (rows a16-a19 of SURVEY §8):
+//   forward_stage  (model.cpp:77-92, affine_tanh :59-73)
+//   backward_stage (model.cpp:94-156)
+//   accumulate_grads / ordered_sum across micro-batches (model.cpp:158-172)
+//   mse_loss gradient (model.cpp:174-188), synth inputs (:190-198)
+//
+// Precision: activations, weights and dz are bf16 GEMM operands; the tensor
+// cores accumulate in fp32; parameter gradients are accumulated in fp32 in
+// ascending micro-batch order (left to right, like ordered_sum).  Results
+// are tolerance-matched to the fp64 reference and bit-reproducible run to
+// run (fixed tiling, no atomics) — the replay-equals-ghost-run contract.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "internal.h"
+#include "umma_gemm_host.h"
+
+namespace rwb {
+namespace {
+
+using bf16 = __nv_bfloat16;
+constexpr int kBN = 256;
+
+__global__ void dtanh_first_kernel(const bf16* __restrict__ g, const bf16* __restrict__ y,
+                                   bf16* __restrict__ dz, uint64_t n) {
+  // dz = dL/dy * (1 - y^2)   (model.cpp:185-192)
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const float yv = __bfloat162float(y[i]);
+    const float d = __fmul_rn(__bfloat162float(g[i]), __fsub_rn(1.f, __fmul_rn(yv, yv)));
+    dz[i] = __float2bfloat16_rn(d);
+  }
+}
+
+// db[c] (+)= sum_r dz[r, c]: fixed two-level order (row splits summed in order)
+constexpr int kColSplit = 64;
+__global__ void colsum_partial_kernel(const bf16* __restrict__ dz, int64_t rows, int64_t cols,
+                                      float* __restrict__ part) {
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int s = blockIdx.y;
+  if (c >= cols) return;
+  const int64_t r0 = rows * s / kColSplit, r1 = rows * (s + 1) / kColSplit;
+  float acc = 0.f;
+  for (int64_t r = r0; r < r1; ++r) acc = __fadd_rn(acc, __bfloat162float(dz[r * cols + c]));
+  part[int64_t(s) * cols + c] = acc;
+}
+__global__ void colsum_final_kernel(const float* __restrict__ part, int64_t cols, float* __restrict__ db,
+                                    int accumulate) {
+  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (c >= cols) return;
+  float acc = part[c];
+  for (int s = 1; s < kColSplit; ++s) acc = __fadd_rn(acc, part[int64_t(s) * cols + c]);
+  db[c] = accumulate ? __fadd_rn(db[c], acc) : acc;
+}
+
+__global__ void cast_f32_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+// mse_loss (model.cpp:174-188): grad = 2/(n*mbs) * (pred - target); the
+// per-block partial loss sums are reduced in block order by a second pass.
+__global__ void mse_grad_kernel(const bf16* __restrict__ pred, const float* __restrict__ target, uint64_t n,
+                                float scale, bf16* __restrict__ grad, double* __restrict__ part) {
+  __shared__ double sh[256];
+  double acc = 0.0;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const float d = __fsub_rn(__bfloat162float(pred[i]), target[i]);
+    grad[i] = __float2bfloat16_rn(__fmul_rn(scale, d));
+    acc += double(d) * double(d);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+__global__ void mse_final_kernel(const double* __restrict__ part, int nparts, uint64_t n, double* loss) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nparts; ++i) s += part[i];
+    *loss = s / double(n);
+  }
+}
+
+int grid1d(uint64_t n) {
+  uint64_t g = (n + 255) / 256;
+  return int(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
+}
+
+}  // namespace
+
+int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, const void* w, const float* b,
+                         void* y, void* stream) {
+  gemm::EpiArgs ep{};
+  ep.out = y;
+  ep.ldo = out;
+  ep.bias = b;
+  // Y[R,out] = X[R,in] . W[in,out]: A = X (K-major), B = W viewed [out,in] (MN-major)
+  return gemm::launch<kBN, gemm::K_MAJOR, gemm::MN_MAJOR, gemm::EPI_BIAS_TANH_BF16>(
+      x, in, w, out, int(rows), int(out), int(in), ep, static_cast<cudaStream_t>(stream));
+}
+
+int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
+                       const void* y_prev, void* dst, void* stream) {
+  gemm::EpiArgs ep{};
+  ep.out = dst;
+  ep.ldo = in;
+  ep.y = static_cast<const bf16*>(y_prev);
+  ep.ldy = in;
+  auto st = static_cast<cudaStream_t>(stream);
+  // dX[R,in] = dZ[R,out] . W[in,out]^T: A = dZ (K-major), B = W as [in,out] (K-major)
+  if (y_prev)
+    return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_DTANH_BF16>(dz, out, w, out, int(rows),
+                                                                                 int(in), int(out), ep, st);
+  return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BF16>(dz, out, w, out, int(rows), int(in),
+                                                                         int(out), ep, st);
+}
+
+int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
+                       int accumulate, void* stream) {
+  gemm::EpiArgs ep{};
+  ep.out = dw;
+  ep.ldo = out;
+  auto st = static_cast<cudaStream_t>(stream);
+  // dW[in,out] = X[R,in]^T . dZ[R,out]: A(m=in,k=r) = X[r,m] (MN-major), B(n=out,k=r) = dZ[r,n] (MN-major)
+  if (accumulate)
+    return gemm::launch<kBN, gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32_ACC>(x, in, dz, out, int(in), int(out),
+                                                                                int(rows), ep, st);
+  return gemm::launch<kBN, gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32>(x, in, dz, out, int(in), int(out),
+                                                                          int(rows), ep, st);
+}
+
+int replay_dtanh_first(const void* g, const void* y, void* dz, uint64_t n, void* stream) {
+  dtanh_first_kernel<<<grid1d(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const bf16*>(g), static_cast<const bf16*>(y), static_cast<bf16*>(dz), n);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int replay_colsum(const void* dz, int64_t rows, int64_t cols, float* db, float* scratch, int accumulate,
+                  void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  dim3 g(unsigned((cols + 127) / 128), kColSplit);
+  colsum_partial_kernel<<<g, 128, 0, st>>>(static_cast<const bf16*>(dz), rows, cols, scratch);
+  colsum_final_kernel<<<unsigned((cols + 127) / 128), 128, 0, st>>>(scratch, cols, db, accumulate);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int replay_cast_bf16(const float* in, void* out, uint64_t n, void* stream) {
+  cast_f32_bf16_kernel<<<grid1d(n), 256, 0, static_cast<cudaStream_t>(stream)>>>(in, static_cast<bf16*>(out), n);
+  return static_cast<int>(cudaGetLastError());
+}
+
+int replay_mse_grad(const void* pred, const float* target, uint64_t n, uint64_t micro_batches, void* grad,
+                    double* loss, double* scratch, void* stream) {
+  auto st = static_cast<cudaStream_t>(stream);
+  const int blocks = 256;
+  const float scale = static_cast<float>(2.0 / (double(n) * double(micro_batches)));
+  mse_grad_kernel<<<blocks, 256, 0, st>>>(static_cast<const bf16*>(pred), target, n, scale,
+                                          static_cast<bf16*>(grad), scratch);
+  if (loss) mse_final_kernel<<<1, 32, 0, st>>>(scratch, blocks, n, loss);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace rwb

@@ -1,0 +1,393 @@
+"""Logging-based replay on the B200.
+
+Reference semantics (model.cpp; recovery.cpp is absent):
+  * a Stage is `num_layers` affine+tanh layers (make_stage, model.cpp:104-126),
+    params in blocks() order W0, b0, W1, b1, ... (model.cpp:84-92);
+  * an iteration runs every micro-batch forward + backward, accumulates the
+    per-micro-batch gradients in ascending micro-batch order (accumulate_grads,
+    model.cpp:230-244) and then steps every block in reverse layer order
+    (apply_layerwise_updates);
+  * recover_replay: the replacement loads the checkpoint and
+    re-executes its stages feeding the logged inbound activations / gradients
+    in timestamp order, applying the optimizer steps identically;
+  * recover_parallel: helper h replays micro-batches
+    {mb : mb mod d == h}; gradients are merged in ascending mb order (bit-exact
+    equivalence with sequential replay), then one step.
+
+Device mapping: fp32 master state (DeviceState, fused step kernels) + bf16
+weight shadows; bf16 activations; tcgen05 GEMMs with fused epilogues
+(csrc/umma_gemm.cuh).  Everything is deterministic, so a replay equals the
+GPU ghost run bit for bit; against the fp64 reference it is tolerance-matched.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import torch
+
+from ._lib import LIB, RwError, check
+from .optim import DeviceState, OptimizerHyper, derive_seed, seeded_fill_
+
+RW_BF16 = 2
+
+
+class rw_stage_desc(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("_pad", C.c_int32), ("dims", C.POINTER(C.c_int64)),
+                ("w", C.POINTER(C.c_void_p)), ("b", C.POINTER(C.c_void_p))]
+
+
+_sig = {
+    "rw_stage_forward": (C.c_int, [C.POINTER(rw_stage_desc), C.c_int64, C.POINTER(C.c_void_p), C.c_void_p]),
+    "rw_stage_backward": (C.c_int, [C.POINTER(rw_stage_desc), C.c_int64, C.POINTER(C.c_void_p), C.c_void_p,
+                                    C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int32,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rw_mse_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p]),
+    "rw_cast_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+}
+for _n, (_r, _a) in _sig.items():
+    _f = getattr(LIB, _n)
+    _f.restype, _f.argtypes = _r, _a
+
+
+def _sh(stream=None) -> C.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _p(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr() if t is not None else None)
+
+
+def synth_inputs(seed: int, iteration: int, stream: int, rows: int, dim: int,
+                 dtype=torch.bfloat16, device=None) -> torch.Tensor:
+    """synth_inputs (model.cpp:262-265): seeded_fill of derive_seed(seed, {1, it, stream})."""
+    out = torch.empty(rows, dim, dtype=dtype, device=device or torch.cuda.current_device())
+    _fill(out, derive_seed(seed, [1, iteration, stream]))
+    return out
+
+
+def synth_targets(seed: int, iteration: int, stream: int, rows: int, dim: int, device=None) -> torch.Tensor:
+    """synth_targets (model.cpp:267-270), fp32."""
+    out = torch.empty(rows, dim, dtype=torch.float32, device=device or torch.cuda.current_device())
+    _fill(out, derive_seed(seed, [2, iteration, stream]))
+    return out
+
+
+def _fill(t: torch.Tensor, seed: int):
+    dt = {torch.float32: 0, torch.float64: 1, torch.bfloat16: RW_BF16}[t.dtype]
+    check(LIB.rw_seeded_fill(dt, _p(t), t.numel(), seed, 0, _sh()))
+
+
+class Stage:
+    """One pipeline stage (model.hpp:24-39) living on one GPU."""
+
+    def __init__(self, stage_id: int, input_dim: int, hidden_dim: int, output_dim: int, num_layers: int,
+                 seed: int, kind: int, device=None):
+        if num_layers < 1:
+            raise RwError(18, "InvalidConfig: stage needs >= 1 layer")
+        self.stage_id = stage_id
+        self.dims = [input_dim] + [hidden_dim] * (num_layers - 1) + [output_dim]
+        self.L = num_layers
+        sizes = []
+        for l in range(num_layers):
+            sizes += [self.dims[l] * self.dims[l + 1], self.dims[l + 1]]
+        self.state = DeviceState(sizes, dtype=torch.float32, kind=kind, device=device)
+        dev = self.state.device
+        self.device = dev
+        # make_stage (model.cpp:117-122): W_l from derive_seed(seed,{id,l,0}), b_l from {id,l,1}
+        for l in range(num_layers):
+            seeded_fill_(self.state.view("x", 2 * l), derive_seed(seed, [stage_id, l, 0]))
+            seeded_fill_(self.state.view("x", 2 * l + 1), derive_seed(seed, [stage_id, l, 1]))
+        self.grad = torch.zeros_like(self.state.x)  # flat, same layout as the state
+        self.w16 = [torch.empty(self.dims[l] * self.dims[l + 1], dtype=torch.bfloat16, device=dev)
+                    for l in range(num_layers)]
+        self.refresh_shadows()
+        self._dims_c = (C.c_int64 * (num_layers + 1))(*self.dims)
+        self._w_c = (C.c_void_p * num_layers)(*[w.data_ptr() for w in self.w16])
+        self._b_c = (C.c_void_p * num_layers)(*[self.state.view("x", 2 * l + 1).data_ptr()
+                                                for l in range(num_layers)])
+        self._dw_c = (C.c_void_p * num_layers)(*[self.grad_view(2 * l).data_ptr() for l in range(num_layers)])
+        self._db_c = (C.c_void_p * num_layers)(*[self.grad_view(2 * l + 1).data_ptr()
+                                                 for l in range(num_layers)])
+        self.desc = rw_stage_desc(num_layers, 0, self._dims_c, self._w_c, self._b_c)
+        self._scratch: dict = {}
+
+    # ---- buffers ----
+    def grad_view(self, i: int) -> torch.Tensor:
+        o, n = self.state.offsets[i], self.state.sizes[i]
+        return self.grad[o:o + n]
+
+    def grad_ptrs(self, flat: torch.Tensor):
+        """dw/db pointer arrays into a flat fp32 buffer laid out like the state."""
+        o = self.state.offsets
+        dw = (C.c_void_p * self.L)(*[flat[o[2 * l]:].data_ptr() for l in range(self.L)])
+        db = (C.c_void_p * self.L)(*[flat[o[2 * l + 1]:].data_ptr() for l in range(self.L)])
+        return dw, db
+
+    def refresh_shadows(self, stream=None):
+        for l in range(self.L):
+            w = self.state.view("x", 2 * l)
+            check(LIB.rw_cast_f32_to_bf16(_p(w), _p(self.w16[l]), w.numel(), _sh(stream)))
+
+    def new_acts(self, rows: int) -> list[torch.Tensor]:
+        return [torch.empty(rows, d, dtype=torch.bfloat16, device=self.device) for d in self.dims]
+
+    def _scr(self, rows: int):
+        if rows not in self._scratch:
+            mx = max(self.dims)
+            self._scratch[rows] = (torch.empty(rows * mx, dtype=torch.bfloat16, device=self.device),
+                                   torch.empty(rows * mx, dtype=torch.bfloat16, device=self.device),
+                                   torch.empty(64 * mx, dtype=torch.float32, device=self.device))
+        return self._scratch[rows]
+
+    # ---- model.cpp entry points ----
+    def forward(self, acts: Sequence[torch.Tensor], stream=None) -> torch.Tensor:
+        """forward_stage: acts[0] is the input; fills acts[1..L]; returns acts[L]."""
+        rows = acts[0].shape[0]
+        arr = (C.c_void_p * (self.L + 1))(*[a.data_ptr() for a in acts])
+        check(LIB.rw_stage_forward(C.byref(self.desc), rows, arr, _sh(stream)))
+        return acts[-1]
+
+    def backward(self, acts: Sequence[torch.Tensor], grad_in: torch.Tensor, grad_out: torch.Tensor | None,
+                 accumulate: bool, dw=None, db=None, stream=None) -> None:
+        """backward_stage + ordered accumulation into self.grad (or dw/db arrays)."""
+        rows = acts[0].shape[0]
+        arr = (C.c_void_p * (self.L + 1))(*[a.data_ptr() for a in acts])
+        s0, s1, sf = self._scr(rows)
+        check(LIB.rw_stage_backward(C.byref(self.desc), rows, arr, _p(grad_in), _p(grad_out),
+                                    dw or self._dw_c, db or self._db_c, int(accumulate), _p(s0), _p(s1),
+                                    _p(sf), _sh(stream)))
+
+    def step(self, hyper: OptimizerHyper, grad: torch.Tensor | None = None, stream=None) -> None:
+        """apply_layerwise_updates over this stage (reverse layer order), then
+        the iteration-end flag clear and the bf16 shadow refresh."""
+        self.state.step(hyper, grad=self.grad if grad is None else grad, stream=stream)
+        self.state.clear_updated(stream=stream)
+        self.refresh_shadows(stream)
+
+    def snapshot(self) -> dict:
+        """In-HBM checkpoint of the stage state (x, m, v, markers)."""
+        return dict(x=self.state.x.clone(), m=None if self.state.m is None else self.state.m.clone(),
+                    v=None if self.state.v is None else self.state.v.clone(), markers=self.state.markers())
+
+    def restore(self, snap: dict) -> None:
+        self.state.x.copy_(snap["x"])
+        if snap["m"] is not None:
+            self.state.m.copy_(snap["m"])
+        if snap["v"] is not None:
+            self.state.v.copy_(snap["v"])
+        self.state.write_markers(snap["markers"])
+        self.refresh_shadows()
+
+
+def mse_grad(pred: torch.Tensor, target: torch.Tensor, micro_batches: int,
+             loss: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """mse_loss gradient (model.cpp:246-260) on the device: bf16 grad, fp64 loss."""
+    grad = torch.empty_like(pred)
+    scratch = torch.empty(256, dtype=torch.float64, device=pred.device)
+    check(LIB.rw_mse_grad(_p(pred), _p(target), pred.numel(), micro_batches, _p(grad), _p(loss), _p(scratch),
+                          _sh(stream)))
+    return grad
+
+
+@dataclass
+class BoundaryLog:
+    """Upstream-backup log of the messages INTO a group of stages:
+    the activation entering its first stage and the gradient entering its last
+    stage, per (iteration, micro-batch), in timestamp order.  Held in HBM or in
+    pinned host memory (north_star)."""
+
+    acts: dict = field(default_factory=dict)    # (it, mb) -> tensor
+    grads: dict = field(default_factory=dict)
+    pinned: bool = False
+
+    def put(self, kind: str, it: int, mb: int, t: torch.Tensor) -> None:
+        if self.pinned:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            t = h
+        else:
+            t = t.clone()
+        (self.acts if kind == "act" else self.grads)[(it, mb)] = t
+
+    def get(self, kind: str, it: int, mb: int, device) -> torch.Tensor | None:
+        d = self.acts if kind == "act" else self.grads
+        t = d.get((it, mb))
+        if t is None:
+            return None
+        return t.to(device, non_blocking=True) if t.device != device else t
+
+    def nbytes(self) -> int:
+        return sum(t.numel() * t.element_size() for d in (self.acts, self.grads) for t in d.values())
+
+
+class Pipeline:
+    """A p-stage pipeline on one GPU used as the failure-free "ghost run"
+    (SPEC:510): same seeds, same kernels.  Logs the boundaries around a group of
+    stages [g0, g1] while training (log_send at group boundaries)."""
+
+    def __init__(self, p: int, dim: int, hidden: int, layers: int, rows: int, micro_batches: int, seed: int,
+                 kind: int, hyper: OptimizerHyper, device=None):
+        self.stages = [Stage(s, dim, hidden, dim, layers, seed, kind, device) for s in range(p)]
+        self.p, self.dim, self.rows, self.m, self.seed, self.hyper = p, dim, rows, micro_batches, seed, hyper
+        self.iteration = 0
+        self.losses: list[float] = []
+
+    def run_iteration(self, log_group: tuple[int, int] | None = None, log: BoundaryLog | None = None) -> float:
+        it = self.iteration
+        dev = self.stages[0].device
+        loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        tot = 0.0
+        for mb in range(self.m):  # timestamp order
+            x = synth_inputs(self.seed, it, mb, self.rows, self.dim, device=dev)
+            all_acts = []
+            for s, st in enumerate(self.stages):
+                acts = st.new_acts(self.rows)
+                acts[0].copy_(x)
+                if log_group and log is not None and s == log_group[0] and s > 0:
+                    log.put("act", it, mb, x)
+                x = st.forward(acts)
+                all_acts.append(acts)
+            tgt = synth_targets(self.seed, it, mb, self.rows, self.dim, device=dev)
+            g = mse_grad(x, tgt, self.m, loss)
+            tot += float(loss.item())
+            for s in range(self.p - 1, -1, -1):
+                if log_group and log is not None and s == log_group[1] and s < self.p - 1:
+                    log.put("grad", it, mb, g)
+                gout = torch.empty(self.rows, self.dim, dtype=torch.bfloat16, device=dev) if s > 0 else None
+                self.stages[s].backward(all_acts[s], g, gout, accumulate=mb > 0)
+                g = gout
+        for st in reversed(self.stages):  # every stage updates after the flush
+            st.step(self.hyper)
+        self.iteration += 1
+        self.losses.append(tot / self.m)
+        return tot / self.m
+
+
+def replay_group(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, rows: int, micro_batches: int,
+                 seed: int, hyper: OptimizerHyper, first: bool, last: bool, dim: int) -> int:
+    """recover_replay of a contiguous group of stages from its
+    checkpoint (already loaded) through iterations [it0, it1): replays every
+    micro-batch in timestamp order from the logged inbound tensors (or the
+    re-derived synthetic inputs / targets at the pipeline ends, which are never
+    logged, model.cpp:190-198).  Returns the number of replayed iterations."""
+    dev = stages[0].device
+    for it in range(it0, it1):
+        for mb in range(micro_batches):
+            if first:
+                x = synth_inputs(seed, it, mb, rows, dim, device=dev)
+            else:
+                x = log.get("act", it, mb, dev)
+                if x is None:
+                    raise RwError(14, f"MissingLogData: activation ({it}, {mb})")
+            all_acts = []
+            for st in stages:
+                acts = st.new_acts(rows)
+                acts[0].copy_(x)
+                x = st.forward(acts)
+                all_acts.append(acts)
+            if last:
+                g = mse_grad(x, synth_targets(seed, it, mb, rows, dim, device=dev), micro_batches)
+            else:
+                g = log.get("grad", it, mb, dev)
+                if g is None:
+                    raise RwError(14, f"MissingLogData: gradient ({it}, {mb})")
+            for k in range(len(stages) - 1, -1, -1):
+                gout = torch.empty(rows, stages[k].dims[0], dtype=torch.bfloat16, device=dev) if k > 0 else None
+                stages[k].backward(all_acts[k], g, gout, accumulate=mb > 0)
+                g = gout
+        for st in reversed(stages):
+            st.step(hyper)
+    return it1 - it0
+
+
+def parallel_assignment(m: int, d: int) -> list[list[int]]:
+    """helper h replays micro-batches {mb : mb mod d == h}."""
+    return [[mb for mb in range(m) if mb % d == h] for h in range(d)]
+
+
+def helper_pass(stages: Sequence[Stage], log: BoundaryLog, it: int, mbs: Sequence[int], rows: int,
+                micro_batches: int, seed: int, first: bool, last: bool, dim: int) -> dict:
+    """One helper's share of iteration `it`: forward + backward of its
+    micro-batches, each into its OWN flat gradient buffers (one per stage), so
+    the merge can restore the ascending-mb order exactly."""
+    dev = stages[0].device
+    out = {}
+    for mb in mbs:
+        if first:
+            x = synth_inputs(seed, it, mb, rows, dim, device=dev)
+        else:
+            x = log.get("act", it, mb, dev)
+            if x is None:
+                raise RwError(14, f"MissingLogData: activation ({it}, {mb})")
+        all_acts = []
+        for st in stages:
+            acts = st.new_acts(rows)
+            acts[0].copy_(x)
+            x = st.forward(acts)
+            all_acts.append(acts)
+        if last:
+            g = mse_grad(x, synth_targets(seed, it, mb, rows, dim, device=dev), micro_batches)
+        else:
+            g = log.get("grad", it, mb, dev)
+            if g is None:
+                raise RwError(14, f"MissingLogData: gradient ({it}, {mb})")
+        bufs = [torch.empty_like(st.grad) for st in stages]
+        for k in range(len(stages) - 1, -1, -1):
+            gout = torch.empty(rows, stages[k].dims[0], dtype=torch.bfloat16, device=dev) if k > 0 else None
+            dw, db = stages[k].grad_ptrs(bufs[k])
+            stages[k].backward(all_acts[k], g, gout, accumulate=False, dw=dw, db=db)
+            g = gout
+        out[mb] = bufs
+    return out
+
+
+def ordered_merge(per_mb: dict, k: int, m: int, group=None) -> torch.Tensor:
+    """Merged gradient of stage k: ordered_sum over micro-batches 0..m-1
+    (SPEC:538).  Without a process group every micro-batch is local.  With one,
+    the flat gradient is sharded over the d ranks: each micro-batch's shard j is
+    scattered from its owner (mb mod d) to rank j, rank j sums its m shards in
+    ascending mb order, and an all-gather rebuilds the full merged gradient on
+    every rank (which then steps redundantly and identically)."""
+    from .optim import ordered_sum
+    import torch.distributed as dist
+    if group is None and not (dist.is_available() and dist.is_initialized()):
+        return ordered_sum([per_mb[mb][k] for mb in range(m)])
+    d = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    any_buf = next(iter(per_mb.values()))[k]
+    P = any_buf.numel()
+    chunk = ((P + d - 1) // d + 63) // 64 * 64
+    pad = chunk * d - P
+    shards = []
+    for mb in range(m):
+        owner = mb % d
+        recv = torch.empty(chunk, dtype=torch.float32, device=any_buf.device)
+        if rank == owner:
+            src = per_mb[mb][k]
+            if pad:
+                src = torch.cat([src, src.new_zeros(pad)])
+            dist.scatter(recv, list(src.split(chunk)), src=owner, group=group)
+        else:
+            dist.scatter(recv, None, src=owner, group=group)
+        shards.append(recv)
+    merged_shard = ordered_sum(shards)
+    full = torch.empty(chunk * d, dtype=torch.float32, device=any_buf.device)
+    dist.all_gather_into_tensor(full, merged_shard, group=group)
+    return full[:P]
+
+
+def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, rows: int,
+                     micro_batches: int, seed: int, hyper: OptimizerHyper, first: bool, last: bool, dim: int,
+                     group=None, rank: int = 0, d: int = 1) -> int:
+    """recover_parallel for this helper rank."""
+    assign = parallel_assignment(micro_batches, d)
+    for it in range(it0, it1):
+        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim)
+        for k, st in enumerate(stages):
+            merged = ordered_merge(per_mb, k, micro_batches, group)
+            st.step(hyper, grad=merged)
+    return it1 - it0

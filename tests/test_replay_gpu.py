@@ -1,0 +1,193 @@
+"""Replay path on the GPU.
+
+Bars:
+  * forward_stage / backward_stage / mse_loss vs the fp64 reference library:
+    relative tolerance (bf16 tensor-core GEMMs, fp32 accumulation):
+    |gpu - ref| <= 3e-2 * max|ref| per tensor (stated in north_star terms:
+    "replay within a stated relative tolerance");
+  * logging replay == failure-free GPU ghost run, BIT FOR BIT (acceptance 4);
+  * parallel recovery (mb mod d, ascending-mb merge) == sequential replay,
+    BIT FOR BIT (acceptance 5), d = 2 emulated on one GPU;
+  * MissingLogData when a needed record is absent.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle.oracle import _dptr
+from paper_2302_06173_b200 import ADAM, SGDM, OptimizerHyper, RwError
+from paper_2302_06173_b200.optim import ordered_sum
+from paper_2302_06173_b200.replay import (BoundaryLog, Pipeline, Stage, helper_pass, mse_grad,
+                                          parallel_assignment, replay_group, synth_inputs, synth_targets)
+
+pytestmark = pytest.mark.gpu
+TOL = 3e-2
+
+
+def _close(gpu, ref, tol=TOL):
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    err = np.max(np.abs(gpu - ref))
+    scale = np.max(np.abs(ref))
+    return err <= tol * scale + 1e-6, (err, scale)
+
+
+def test_stage_forward_backward_vs_reference(ref):
+    torch.manual_seed(0)
+    sid, din, dh, dout, L, seed, rows = 1, 64, 128, 64, 2, 2302, 256
+    st = Stage(sid, din, dh, dout, L, seed, ADAM)
+    rs = ref.L.ref_stage_make(sid, din, dh, dout, L, seed)
+    assert rs
+    # identical initial parameters (fp32 master = single rounding of the reference's fp64)
+    for bi in range(2 * L):
+        blk = ref.L.ref_stage_block(rs, bi)
+        n = st.state.sizes[bi]
+        xr = np.empty(n)
+        ref.L.ref_block_get(C.c_void_p(blk), _dptr(xr), None, None, None, None, None)
+        assert np.array_equal(st.state.view("x", bi).cpu().numpy(), xr.astype(np.float32))
+    x = synth_inputs(seed, 0, 0, rows, din)
+    acts = st.new_acts(rows)
+    acts[0].copy_(x)
+    y = st.forward(acts)
+    xin = x.float().cpu().numpy().astype(np.float64)
+    yref = np.empty(rows * dout)
+    assert ref.L.ref_forward_stage(rs, _dptr(np.ascontiguousarray(xin.ravel())), rows, din, 0, _dptr(yref)) == 0
+    ok, info = _close(y.float().cpu().numpy().ravel(), yref)
+    assert ok, info
+    # backward: upstream gradient = mse grad against synthetic targets
+    tgt = synth_targets(seed, 0, 0, rows, dout)
+    g = mse_grad(y, tgt, 4)
+    gref = np.empty(rows * dout)
+    loss = C.c_double()
+    assert ref.L.ref_mse_loss(_dptr(yref), _dptr(np.ascontiguousarray(tgt.cpu().numpy().astype(np.float64).ravel())),
+                              rows, dout, 4, C.byref(loss), _dptr(gref)) == 0
+    ok, info = _close(g.float().cpu().numpy().ravel(), gref)
+    assert ok, info
+    gin = np.ascontiguousarray(g.float().cpu().numpy().astype(np.float64).ravel())  # same upstream for both
+    gout = torch.empty(rows, din, dtype=torch.bfloat16, device="cuda")
+    st.backward(acts, g, gout, accumulate=False)
+    gout_ref = np.empty(rows * din)
+    pg = [np.empty(n) for n in st.state.sizes]
+    parr = (C.POINTER(C.c_double) * len(pg))(*[_dptr(a) for a in pg])
+    assert ref.L.ref_backward_stage(rs, _dptr(gin), rows, dout, 0, _dptr(gout_ref), parr) == 0
+    ok, info = _close(gout.float().cpu().numpy().ravel(), gout_ref)
+    assert ok, ("grad_out", info)
+    for bi in range(2 * L):
+        ok, info = _close(st.grad_view(bi).cpu().numpy(), pg[bi])
+        assert ok, (bi, info)
+    ref.L.ref_stage_free(rs)
+
+
+def test_backward_is_deterministic():
+    st = Stage(0, 64, 128, 64, 2, 7, ADAM)
+    x = synth_inputs(7, 0, 0, 256, 64)
+    acts = st.new_acts(256)
+    acts[0].copy_(x)
+    st.forward(acts)
+    g = synth_inputs(7, 0, 1, 256, 64)
+    outs = []
+    for _ in range(3):
+        gout = torch.empty(256, 64, dtype=torch.bfloat16, device="cuda")
+        st.backward(acts, g, gout, accumulate=False)
+        outs.append((gout.clone(), st.grad.clone()))
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+
+
+def _pipeline(kind=ADAM):
+    h = OptimizerHyper(kind=kind, lr=1e-3 if kind == ADAM else 0.05, weight_decay=0.01)
+    return Pipeline(p=3, dim=64, hidden=128, layers=2, rows=128, micro_batches=4, seed=11, kind=kind,
+                    hyper=h), h
+
+
+@pytest.mark.parametrize("kind", [ADAM, SGDM])
+def test_logging_replay_equals_ghost_run_bitwise(kind):
+    """§7 scenario at desk scale: checkpoint at it 2, failure at it 5, stage 1
+    (a middle stage) replayed from logs -> bit-identical to the ghost run."""
+    ghost, h = _pipeline(kind)
+    log = BoundaryLog()
+    snaps = {}
+    for it in range(5):
+        if it == 2:
+            snaps = ghost.stages[1].snapshot()  # global checkpoint of the failed stage
+        ghost.run_iteration(log_group=(1, 1), log=log)
+    assert len(log.acts) == 5 * 4 and len(log.grads) == 5 * 4
+    # replacement: fresh stage, load checkpoint, replay iterations 2..4
+    rep = Stage(1, 64, 128, 64, 2, 11, kind)
+    rep.restore(snaps)
+    n = replay_group([rep], log, 2, 5, 128, 4, 11, h, first=False, last=False, dim=64)
+    assert n == 3
+    g = ghost.stages[1].state
+    for name in ("x", "m", "v"):
+        a, b = getattr(rep.state, name), getattr(g, name)
+        if a is None:
+            continue
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32)), name
+    assert rep.state.markers() == g.markers()
+
+
+def test_group_replay_last_stages_bitwise():
+    ghost, h = _pipeline()
+    log = BoundaryLog(pinned=True)  # logs in pinned host memory
+    for it in range(3):
+        if it == 1:
+            s1, s2 = ghost.stages[1].snapshot(), ghost.stages[2].snapshot()
+        ghost.run_iteration(log_group=(1, 2), log=log)
+    assert len(log.grads) == 0  # the last stage's gradient comes from the loss, never logged
+    a, b = Stage(1, 64, 128, 64, 2, 11, ADAM), Stage(2, 64, 128, 64, 2, 11, ADAM)
+    a.restore(s1)
+    b.restore(s2)
+    replay_group([a, b], log, 1, 3, 128, 4, 11, h, first=False, last=True, dim=64)
+    assert torch.equal(a.state.x, ghost.stages[1].state.x)
+    assert torch.equal(b.state.x, ghost.stages[2].state.x)
+    assert torch.equal(b.state.v, ghost.stages[2].state.v)
+
+
+def test_parallel_recovery_equals_sequential_bitwise():
+    ghost, h = _pipeline()
+    log = BoundaryLog()
+    for it in range(3):
+        if it == 1:
+            snap = ghost.stages[1].snapshot()
+        ghost.run_iteration(log_group=(1, 1), log=log)
+    seq = Stage(1, 64, 128, 64, 2, 11, ADAM)
+    seq.restore(snap)
+    replay_group([seq], log, 1, 3, 128, 4, 11, h, first=False, last=False, dim=64)
+    # d = 2 helpers (emulated in-process): Fig 6 assignment {0,2} / {1,3}
+    assert parallel_assignment(4, 2) == [[0, 2], [1, 3]]
+    helpers = [Stage(1, 64, 128, 64, 2, 11, ADAM) for _ in range(2)]
+    for hs in helpers:
+        hs.restore(snap)
+    for it in range(1, 3):
+        per_mb = {}
+        for r, hs in enumerate(helpers):
+            per_mb.update(helper_pass([hs], log, it, parallel_assignment(4, 2)[r], 128, 4, 11, False, False, 64))
+        merged = ordered_sum([per_mb[mb][0] for mb in range(4)])
+        for hs in helpers:
+            hs.step(h, grad=merged)
+    for hs in helpers:
+        assert torch.equal(hs.state.x, seq.state.x)
+        assert torch.equal(hs.state.m, seq.state.m)
+        assert torch.equal(hs.state.v, seq.state.v)
+    assert torch.equal(seq.state.x, ghost.stages[1].state.x)
+
+
+def test_missing_log_raises():
+    ghost, h = _pipeline()
+    log = BoundaryLog()
+    snap = ghost.stages[1].snapshot()
+    ghost.run_iteration(log_group=(1, 1), log=log)
+    del log.grads[(0, 2)]
+    rep = Stage(1, 64, 128, 64, 2, 11, ADAM)
+    rep.restore(snap)
+    with pytest.raises(RwError) as e:
+        replay_group([rep], log, 0, 1, 128, 4, 11, h, first=False, last=False, dim=64)
+    assert e.value.name == "MissingLogData"
+
+
+def test_training_loss_decreases():
+    ghost, h = _pipeline()
+    losses = [ghost.run_iteration() for _ in range(8)]
+    assert all(np.isfinite(losses)) and losses[-1] < losses[0]
