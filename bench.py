@@ -371,6 +371,62 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
                 nvlink_roofline_ms=round(nbytes / 770e9 * 1e3, 3) if nbytes else None)
 
 
+def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 16384, m: int = 8,
+                 dims=(4096, 16384, 4096)) -> dict:
+    """Config 4: logging-based replay of one failed pipeline stage (two
+    affine+tanh layers 4096 -> 16384 -> 4096, micro-batch 8 x 2048 tokens =
+    16384 rows, m = 8 micro-batches, Adam) from logged boundary activations /
+    gradients resident in HBM, spread over the `world` GPUs as parallel
+    recovery (helper h replays mb with mb mod d == h; ascending-mb merge).
+    Times `iters` replayed iterations end to end (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import ADAM, OptimizerHyper
+    from paper_2302_06173_b200.replay import BoundaryLog, Stage, recover_parallel, replay_group, synth_inputs
+    h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
+    st = Stage(3, dims[0], dims[1], dims[2], 2, 2302, ADAM, device=device.index)
+    log = BoundaryLog()
+    mine = [mb for mb in range(m) if mb % world == rank]
+    for mb in mine:  # synthetic logged tensors for this helper's micro-batches
+        a = synth_inputs(5, 0, mb, rows, dims[0])
+        g = synth_inputs(6, 0, mb, rows, dims[-1]).mul_(1e-3)
+        for it in range(iters + 1):
+            log.acts[(it, mb)] = a
+            log.grads[(it, mb)] = g
+    flop_mb = 2 * rows * (dims[0] * dims[1] + dims[1] * dims[2]) * 2 + 2 * rows * dims[1] * dims[2]
+
+    def run(it0, it1):
+        if world > 1:
+            return recover_parallel([st], log, it0, it1, rows, m, 2302, h, first=False, last=False,
+                                    dim=dims[0], rank=rank, d=world)
+        return replay_group([st], log, it0, it1, rows, m, 2302, h, first=False, last=False, dim=dims[0])
+
+    run(0, 1)  # warm-up (also JIT-free: TMA maps, smem attributes)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run(1, 1 + iters)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    tflops = flop_mb * m * iters / (ms_max * 1e-3) / 1e12
+    del st, log
+    torch.cuda.empty_cache()
+    return dict(workload="config 4: replay of one failed stage (4096->16384->4096 affine+tanh, Adam), "
+                         f"{m} micro-batches x {rows} rows, logs in HBM, parallel recovery over {world} GPU(s)",
+                iterations=iters, ms_per_iteration=round(ms_max / iters, 3),
+                tflops_aggregate=round(tflops, 1), tflop_per_iteration=round(flop_mb * m / 1e12, 2),
+                frac_of_bf16_peak_aggregate=round(tflops / (1649.8 * world), 4),
+                gemm="tcgen05 kind::f16 M128xN256xK16, TMA SW128, TMEM double-buffered accumulators")
+
+
 def run_b200(args) -> None:
     import torch
     import torch.distributed as dist
@@ -435,6 +491,12 @@ def run_b200(args) -> None:
                 extras["recovery"] = recovery_e2e(world, rank, device)
             except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
                 extras["recovery"] = {"error": f"OOM: {e}"}
+            torch.cuda.empty_cache()
+            if not args.no_replay:
+                try:
+                    extras["replay"] = replay_bench(world, rank, device, iters=args.replay_iters)
+                except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
+                    extras["replay"] = {"error": f"OOM: {e}"}
     clocks = clk.summary()
     if rank != 0:
         if world > 1:
@@ -488,6 +550,8 @@ def main():
     ap.add_argument("--config", default="adam340m", choices=["adam340m", "adam1b", "sgdm10m"])
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-replay", action="store_true")
+    ap.add_argument("--replay-iters", type=int, default=2)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
