@@ -329,19 +329,49 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
             __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + int64_t(row) * ep.ldo + col0;
+            const bool full = col0 + 32 <= N;
             float w[32];
+            if constexpr (EPI == EPI_BIAS_TANH_BF16) {
+              float bv[32];
+              if (full) {  // same 128 B for every lane of the warp: one broadcast transaction each
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              float a = v[j];
-              if constexpr (EPI == EPI_BIAS_TANH_BF16) {
-                const float b = (col0 + j < N) ? __ldg(ep.bias + col0 + j) : 0.f;
-                a = tanhf(__fadd_rn(a, b));
-              } else if constexpr (EPI == EPI_DTANH_BF16) {
-                float yv = 0.f;
-                if (col0 + j < N) yv = __bfloat162float(ep.y[int64_t(row) * ep.ldy + col0 + j]);
-                a = __fmul_rn(a, __fsub_rn(1.f, __fmul_rn(yv, yv)));
+                for (int j = 0; j < 32; j += 4) {
+                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j));
+                  bv[j] = b4.x;
+                  bv[j + 1] = b4.y;
+                  bv[j + 2] = b4.z;
+                  bv[j + 3] = b4.w;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) bv[j] = (col0 + j < N) ? __ldg(ep.bias + col0 + j) : 0.f;
               }
-              w[j] = a;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) w[j] = tanhf(__fadd_rn(v[j], bv[j]));
+            } else if constexpr (EPI == EPI_DTANH_BF16) {
+              const __nv_bfloat16* yp = ep.y + int64_t(row) * ep.ldy + col0;
+              float yv[32];
+              if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads
+#pragma unroll
+                for (int j = 0; j < 32; j += 8) {
+                  const uint4 u = *reinterpret_cast<const uint4*>(yp + j);
+                  const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(p2[q]);
+                    yv[j + 2 * q] = f.x;
+                    yv[j + 2 * q + 1] = f.y;
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) yv[j] = (col0 + j < N) ? __bfloat162float(yp[j]) : 0.f;
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) w[j] = __fmul_rn(v[j], __fsub_rn(1.f, __fmul_rn(yv[j], yv[j])));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) w[j] = v[j];
             }
             if (col0 + 32 <= N) {
 #pragma unroll

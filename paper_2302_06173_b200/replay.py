@@ -85,11 +85,18 @@ class Stage:
     """One pipeline stage (model.hpp:24-39) living on one GPU."""
 
     def __init__(self, stage_id: int, input_dim: int, hidden_dim: int, output_dim: int, num_layers: int,
-                 seed: int, kind: int, device=None):
+                 seed: int, kind: int, device=None, dims: Sequence[int] | None = None):
+        """make_stage(stage_id, input_dim, hidden_dim, output_dim, num_layers, seed)
+        (model.cpp:104-126).  `dims` (num_layers + 1 widths) generalises the
+        uniform hidden width, e.g. MLP blocks 4096 -> 11008 -> 4096 -> ..."""
         if num_layers < 1:
             raise RwError(18, "InvalidConfig: stage needs >= 1 layer")
         self.stage_id = stage_id
         self.dims = [input_dim] + [hidden_dim] * (num_layers - 1) + [output_dim]
+        if dims is not None:
+            if len(dims) != num_layers + 1:
+                raise RwError(2, "ShapeMismatch: dims must have num_layers + 1 entries")
+            self.dims = [int(d) for d in dims]
         self.L = num_layers
         sizes = []
         for l in range(num_layers):
