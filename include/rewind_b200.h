@@ -153,6 +153,21 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* group_ids,
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
                       void* stream);
 
+/* ---- replica recovery fused with the undo ----
+ * CUDA IPC export/import of a device buffer so a survivor can write into a
+ * replacement's HBM over NVLink.  export returns the 64-byte handle of the
+ * enclosing allocation and the byte offset of ptr inside it. */
+int rw_ipc_export(const void* ptr, void* handle_out /*64 bytes*/, uint64_t* offset_out);
+int rw_ipc_import(const void* handle /*64 bytes*/, void** base_out);
+int rw_ipc_close(void* base);
+/* apply_undo fused with recover_replication: undoes undo_ids in place and, in
+ * the same kernel, streams every group of the resolved state (x, m, v; g too
+ * when peer_g != NULL) into the peer replica's buffers (same layout) with
+ * NVLink bulk stores.  Guards as rw_optimizer_undo.  The peer's markers are
+ * the caller's to set (they equal the survivor's after the call). */
+int rw_undo_and_push(rw_state* s, const rw_hyper* h, const uint32_t* undo_ids, uint32_t n_undo,
+                     void* peer_x, void* peer_g, void* peer_m, void* peer_v, void* stream);
+
 /* ---- host-buffer entry points: ONE reference ParamBlock held in host memory ----
  * Exactly optimizer_step / optimizer_undo (optim.cpp:338-385) on a block whose
  * x, g, m, v (and AMSGrad vmax) live in host memory: the library stages them

@@ -105,6 +105,13 @@ def _load() -> C.CDLL:
         "rw_recovery_time_estimate": (C.c_int, [u32, P(dbl), P(dbl), dbl, i32, P(u32), dbl,
                                                 P(dbl)]),
         "rw_logging_worthwhile": (C.c_int, [dbl, dbl, i32, i32, dbl, P(i32), P(dbl), P(dbl)]),
+        "rw_ipc_export": (C.c_int, [vp, vp, P(u64)]),
+        "rw_ipc_import": (C.c_int, [vp, P(vp)]),
+        "rw_ipc_close": (C.c_int, [vp]),
+        "rw_undo_and_push": (C.c_int, [vp, P(rw_hyper), P(u32), u32, vp, vp, vp, vp, vp]),
+        "rw_host_block_step": (C.c_int, [i32, vp, vp, vp, vp, vp, u64, P(u64), P(u32), vp,
+                                         P(rw_hyper)]),
+        "rw_host_block_undo": (C.c_int, [i32, vp, vp, vp, vp, u64, P(u64), P(u32), P(rw_hyper)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -16,7 +16,10 @@ struct WorkItem {
   uint32_t chunk_begin;  // first global chunk index of this group
   uint32_t nchunks;
   uint32_t sidx;         // index into the ScalarSet table
+  uint32_t flags;        // kWorkCopyOnly: pass the group through (push only)
+  uint32_t pad;
 };
+constexpr uint32_t kWorkCopyOnly = 1u;
 
 // t-dependent scalars of one call, derived in double on the host exactly as
 // optim.cpp does (lr_at :128-135, bias_correction :172-175, denom :184/:255).
@@ -49,6 +52,11 @@ struct LaunchArgs {
   Uniform u;
   rw_group* groups;
   uint32_t* done;
+  // fused replica push (rw_undo_and_push): peer buffers, same layout; null = off
+  void* px = nullptr;
+  void* pg = nullptr;
+  void* pm = nullptr;
+  void* pv = nullptr;
 };
 
 // record the thread-local last-error message (rw_last_error_message)

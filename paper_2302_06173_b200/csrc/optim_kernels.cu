@@ -216,6 +216,8 @@ struct StageMeta {
   uint32_t item;   // work item index
   uint32_t gid;    // group (marker table index)
   uint32_t bad;    // non-finite seen in this tile
+  uint32_t copy;   // copy-only tile (fused push of an untouched group)
+  uint32_t pad;
   ScalarSet ss;    // eta, c1, c2, denom of the tile's group
 };
 
@@ -224,12 +226,16 @@ constexpr size_t dyn_smem_bytes() {
   return size_t(kStages) * Uses<KIND>::slots * kSlotBytes;
 }
 
-template <typename T, int KIND, bool UNDO, bool COPY_GRAD>
+// PUSH: the resolved tiles are also written to a peer replica (NVLink stores
+// from the same bulk-copy engine), and copy-only work items pass untouched
+// groups through to the peer: recover_replication fused with apply_undo.
+template <typename T, int KIND, bool UNDO, bool COPY_GRAD, bool PUSH>
 __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     T* __restrict__ x, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v,
     T* __restrict__ vmax, const T* __restrict__ grad, const WorkItem* __restrict__ work,
     uint32_t n_work, uint32_t total_chunks, const ScalarSet* __restrict__ sets, Uniform u,
-    rw_group* __restrict__ groups, uint32_t* __restrict__ done) {
+    rw_group* __restrict__ groups, uint32_t* __restrict__ done, T* __restrict__ px,
+    T* __restrict__ pg, T* __restrict__ pm, T* __restrict__ pv) {
   using A = Arith<T>;
   using V = typename A::V;
   constexpr int EV = A::EV;
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
   const uint32_t c_end = min(total_chunks, c_begin + per_cta);
 
   // producer-only state (thread 0): cached current work item
-  uint32_t cur = 0, cur_cb = 0, cur_nc = 0, cur_gid = 0;
+  uint32_t cur = 0, cur_cb = 0, cur_nc = 0, cur_gid = 0, cur_flags = 0;
   uint64_t cur_off = 0, cur_len = 0;
   ScalarSet cur_ss{};
   auto load_item = [&](uint32_t i) {
@@ -275,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     cur_off = it.off;
     cur_len = it.len;
     cur_gid = it.gid;
+    cur_flags = it.flags;
     cur_ss = sets[it.sidx];
   };
 
@@ -312,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     mt.item = cur;
     mt.gid = cur_gid;
     mt.bad = 0;
+    mt.copy = (PUSH && (cur_flags & kWorkCopyOnly)) ? 1u : 0u;
     mt.ss = cur_ss;
     const uint32_t bytes = mt.nbulk * sizeof(T);
     constexpr int nload = 2 + (U::m ? 1 : 0) + (U::v ? 1 : 0) + (U::vmax ? 1 : 0);
@@ -330,8 +338,12 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
   uint32_t acc_item = 0xFFFFFFFFu, acc_cnt = 0;
   auto flush = [&]() {
     if (acc_cnt == 0) return;
-    __threadfence();
     const WorkItem& it = work[acc_item];
+    if (PUSH && (it.flags & kWorkCopyOnly)) {  // untouched group: marker unchanged
+      acc_cnt = 0;
+      return;
+    }
+    __threadfence();
     const uint32_t prev = atomicAdd(&done[acc_item], acc_cnt);
     if (prev + acc_cnt == it.nchunks) {
       groups[it.gid].t = it.new_t;
@@ -403,7 +415,10 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
       if constexpr (U::v) *reinterpret_cast<V*>(vs + e) = vr;
       if constexpr (U::vmax) *reinterpret_cast<V*>(ws + e) = wr;
     };
-    if (nbulk == TILE) {  // full tile: compile-time trip count, unrolled for ILP
+    const bool copy_only = PUSH && mt.copy;
+    if (copy_only) {
+      // untouched group: the loaded tile goes to the peer unchanged
+    } else if (nbulk == TILE) {  // full tile: compile-time trip count, unrolled for ILP
       constexpr uint32_t kIters = TILE / (kThreads * EV);
 #pragma unroll
       for (uint32_t k = 0; k < kIters; ++k) body(tid * EV + k * kThreads * EV);
@@ -411,7 +426,13 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
       for (uint32_t e = tid * EV; e < nbulk; e += kThreads * EV) body(e);
     }
     // unaligned head/tail elements straight from global memory
-    if (tid < nhead + ntail) {
+    if (copy_only && tid < nhead + ntail) {
+      const uint64_t i = tid < nhead ? ma + tid : ma16 + nbulk + (tid - nhead);
+      px[i] = x[i];
+      if (pg) pg[i] = g[i];
+      if constexpr (U::m) pm[i] = m[i];
+      if constexpr (U::v) pv[i] = v[i];
+    } else if (tid < nhead + ntail) {
       const uint64_t i = tid < nhead ? ma + tid : ma16 + nbulk + (tid - nhead);
       T xe = x[i];
       const T ge = gsrc[i];
@@ -431,6 +452,12 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
         v[i] = ve;
       }
       if constexpr (U::vmax) vmax[i] = we;
+      if constexpr (PUSH) {
+        px[i] = xe;
+        if (pg) pg[i] = ge;
+        if constexpr (U::m) pm[i] = me;
+        if constexpr (U::v) pv[i] = ve;
+      }
     }
     if (bad) atomicOr(&meta[st].bad, 1u);
     fence_proxy_async_smem();  // generic smem writes -> visible to the bulk stores
@@ -438,11 +465,19 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     if (tid == 0) {
       if (nbulk) {
         const uint32_t bytes = nbulk * sizeof(T);
-        bulk_store(x + ma16, xs, bytes);
-        if constexpr (COPY_GRAD) bulk_store(g + ma16, gs, bytes);
-        if constexpr (U::m) bulk_store(m + ma16, ms, bytes);
-        if constexpr (U::v) bulk_store(v + ma16, vs, bytes);
-        if constexpr (U::vmax) bulk_store(vmax + ma16, ws, bytes);
+        if (!copy_only) {
+          bulk_store(x + ma16, xs, bytes);
+          if constexpr (COPY_GRAD) bulk_store(g + ma16, gs, bytes);
+          if constexpr (U::m) bulk_store(m + ma16, ms, bytes);
+          if constexpr (U::v) bulk_store(v + ma16, vs, bytes);
+          if constexpr (U::vmax) bulk_store(vmax + ma16, ws, bytes);
+        }
+        if constexpr (PUSH) {  // NVLink: the peer replica receives the resolved tile
+          bulk_store(px + ma16, xs, bytes);
+          if (pg) bulk_store(pg + ma16, gs, bytes);
+          if constexpr (U::m) bulk_store(pm + ma16, ms, bytes);
+          if constexpr (U::v) bulk_store(pv + ma16, vs, bytes);
+        }
       }
       bulk_commit();
       if (mt.bad) atomicOr(&groups[mt.gid].flags, 1u);
@@ -464,9 +499,9 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
   }
 }
 
-template <typename T, int KIND, bool UNDO, bool COPY_GRAD>
+template <typename T, int KIND, bool UNDO, bool COPY_GRAD, bool PUSH = false>
 int launch_t(const LaunchArgs& a, cudaStream_t st) {
-  auto kern = optim_kernel<T, KIND, UNDO, COPY_GRAD>;
+  auto kern = optim_kernel<T, KIND, UNDO, COPY_GRAD, PUSH>;
   constexpr size_t smem = dyn_smem_bytes<T, KIND>();
   static int blocks_per_sm = -1;  // per instantiation
   static int num_sms = -1;
@@ -486,7 +521,9 @@ int launch_t(const LaunchArgs& a, cudaStream_t st) {
   kern<<<grid, kThreads, smem, st>>>(static_cast<T*>(a.x), static_cast<T*>(a.g),
                                      static_cast<T*>(a.m), static_cast<T*>(a.v),
                                      static_cast<T*>(a.vmax), static_cast<const T*>(a.grad), a.work,
-                                     a.n_work, a.total_chunks, a.sets, a.u, a.groups, a.done);
+                                     a.n_work, a.total_chunks, a.sets, a.u, a.groups, a.done,
+                                     static_cast<T*>(a.px), static_cast<T*>(a.pg), static_cast<T*>(a.pm),
+                                     static_cast<T*>(a.pv));
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -497,6 +534,7 @@ int launch_kind(const LaunchArgs& a, cudaStream_t st) {
     if constexpr (KIND == RW_AMSGRAD || KIND == RW_LAMB) {
       return static_cast<int>(cudaErrorInvalidValue);
     } else {
+      if (a.px) return launch_t<T, KIND, true, false, true>(a, st);
       return launch_t<T, KIND, true, false>(a, st);
     }
   }

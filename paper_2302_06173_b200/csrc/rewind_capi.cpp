@@ -163,7 +163,8 @@ rwb::ScalarSet scalars_at(const rw_hyper* h, uint64_t tt, double eta) {
 }
 
 int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, bool undo,
-                  const void* grad, const std::vector<double>& etas, void* stream) {
+                  const void* grad, const std::vector<double>& etas, void* stream,
+                  const uint8_t* copy_only = nullptr, void* const* peers = nullptr) {
   if (n == 0) return RW_OK;
   RW_CUDA(cudaSetDevice(s->device));
   Slot& sl = s->slots[s->next_slot];
@@ -200,6 +201,8 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     w.nchunks = static_cast<uint32_t>((gr.len + ce - 1) / ce);
     w.chunk_begin = static_cast<uint32_t>(chunk);
     w.sidx = set_of[undo ? gr.t : gr.t + 1];
+    w.flags = (copy_only && copy_only[i]) ? rwb::kWorkCopyOnly : 0u;
+    w.pad = 0;
     chunk += w.nchunks;
   }
   if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one call");
@@ -227,11 +230,18 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     a.u = uniform_of(h);
     a.groups = s->d_groups;
     a.done = sl.d_done;
+    if (peers) {
+      a.px = peers[0];
+      a.pg = peers[1];
+      a.pm = peers[2];
+      a.pv = peers[3];
+    }
     int e = rwb::launch_optim(a, stream);
     if (e) return cuda_fail(static_cast<cudaError_t>(e), "optim kernel launch");
   }
   // host mirror follows what the kernel writes at group completion
   for (uint32_t i = 0; i < n; ++i) {
+    if (copy_only && copy_only[i]) continue;
     rw_group& gr = s->mirror[ids[i]];
     gr.t = undo ? gr.t - 1 : gr.t + 1;
     gr.updated = undo ? 0u : 1u;
@@ -674,6 +684,102 @@ int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64
   *t -= 1;  // optim.cpp:380-381
   *updated = 0;
   return rw_state_check(S.st, S.stream);  // :382-384, after mutation
+}
+
+}  // extern "C"
+
+// ---------------- peer memory (CUDA IPC over NVLink) ----------------
+#include <cuda.h>
+
+namespace {
+using AddrRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<AddrRangeFn>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+extern "C" {
+
+int rw_ipc_export(const void* ptr, void* handle_out, uint64_t* offset_out) {
+  if (!ptr || !handle_out || !offset_out) return fail(RW_INVALID_ARGUMENT, "null argument");
+  AddrRangeFn fn = addr_range_fn();
+  if (!fn) return fail(RW_CUDA_ERROR, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(RW_CUDA_ERROR, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  RW_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = reinterpret_cast<uint64_t>(ptr) - static_cast<uint64_t>(base);
+  return RW_OK;
+}
+
+int rw_ipc_import(const void* handle, void** base_out) {
+  if (!handle || !base_out) return fail(RW_INVALID_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  RW_CUDA(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return RW_OK;
+}
+
+int rw_ipc_close(void* base) {
+  RW_CUDA(cudaIpcCloseMemHandle(base));
+  return RW_OK;
+}
+
+// apply_undo fused with recover_replication:
+// one launch undoes `undo_ids` in place AND streams every group of the
+// resolved state (x, m, v; g when peer_g) into a peer replica over NVLink.
+int rw_undo_and_push(rw_state* s, const rw_hyper* h, const uint32_t* undo_ids, uint32_t n_undo, void* peer_x,
+                     void* peer_g, void* peer_m, void* peer_v, void* stream) {
+  if (!s || !h || !peer_x || (n_undo && !undo_ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
+  const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW;
+  if ((um && !peer_m) || (uv && !peer_v)) return fail(RW_INVALID_ARGUMENT, "peer m/v buffers required");
+  const uint32_t G = static_cast<uint32_t>(s->mirror.size());
+  std::vector<uint8_t> is_undo(G, 0);
+  std::vector<double> etas_u(n_undo);
+  for (uint32_t i = 0; i < n_undo; ++i) {
+    if (undo_ids[i] >= G) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", undo_ids[i]);
+    if (is_undo[undo_ids[i]]) return fail(RW_INVALID_ARGUMENT, "group id %u listed twice", undo_ids[i]);
+    is_undo[undo_ids[i]] = 1;
+  }
+  // the undo guards of rw_optimizer_undo, same order, before any launch
+  for (uint32_t i = 0; i < n_undo; ++i) {
+    const rw_group& gr = s->mirror[undo_ids[i]];
+    if (!gr.updated) return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: block has no pending update (group %u)", undo_ids[i]);
+    if (h->kind == RW_AMSGRAD) return fail(RW_NOT_INVERTIBLE, "NotInvertible: amsgrad element-wise max has no inverse");
+    int st = lr_at(h, gr.t, &etas_u[i]);
+    if (st) return st;
+    if (h->kind == RW_SGDM && h->momentum == 0.0)
+      return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: momentum == 0 for sgdm");
+    if ((h->kind == RW_ADAM || h->kind == RW_ADAMW) && (h->beta1 == 0.0 || h->beta2 == 0.0))
+      return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0");
+    if ((h->kind == RW_SGD || h->kind == RW_ADAMW) && 1.0 - etas_u[i] * h->weight_decay == 0.0)
+      return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1");
+    if (h->kind == RW_LAMB) return fail(RW_INVALID_ARGUMENT, "lamb is not on the B200 path yet");
+  }
+  // every group, in layout order: undo groups flagged, the rest copy-only
+  std::vector<uint32_t> ids(G);
+  std::vector<uint8_t> copy(G);
+  std::vector<double> etas(G, 0.0);
+  uint32_t k = 0;
+  for (uint32_t gi = 0; gi < G; ++gi) {
+    ids[gi] = gi;
+    copy[gi] = is_undo[gi] ? 0 : 1;
+  }
+  for (uint32_t i = 0; i < n_undo; ++i) etas[undo_ids[i]] = etas_u[i];
+  (void)k;
+  void* peers[4] = {peer_x, peer_g, peer_m, peer_v};
+  return launch_groups(s, h, ids.data(), G, true, nullptr, etas, stream, copy.data(), peers);
 }
 
 }  // extern "C"

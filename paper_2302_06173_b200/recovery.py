@@ -126,6 +126,69 @@ def apply_resolution(state, hyper, plan: ResolvePlan, grad: torch.Tensor | None 
         state.step(hyper, order, grad=grad, stream=stream)
 
 
+def _export(t: torch.Tensor) -> tuple[bytes, int]:
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64()
+    check(LIB.rw_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off)))
+    return bytes(h), off.value
+
+
+def recover_replication_fused(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False,
+                              group=None, stream=None) -> int:
+    """apply_undo + recover_replication in ONE kernel on the survivor `src`:
+    the undo of plan.undo_ids is computed tile by tile and every resolved tile
+    (and every untouched group) is written straight into each replacement's
+    HBM over NVLink (CUDA IPC-mapped peer buffers, bulk stores from the same
+    kernel) — the transfer hides the undo.  Replacements only publish their
+    buffers and wait.  Returns bytes written per replacement."""
+    if not (dist.is_available() and dist.is_initialized()):
+        raise RwError(17, "NoReplica: no process group")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    names = ["x"] + (["g"] if include_grad else []) + [n for n in ("m", "v") if getattr(state, n) is not None]
+    mine = None if rank == src else {n: _export(getattr(state, n)) for n in names}
+    allh: list = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    nbytes = sum(getattr(state, n).numel() * getattr(state, n).element_size() for n in names)
+    if rank == src:
+        h = hyper.to_c() if hasattr(hyper, "to_c") else hyper
+        sh = C.c_void_p((stream or torch.cuda.current_stream()).cuda_stream)
+        undo = [i for i, a in enumerate(plan.actions) if a == ACT_UNDO] if plan.strategy == "Undo" else []
+        if undo:  # the spec-gap re-arm of apply_resolution (decide on t, flag cleared at iteration end)
+            mk = state.markers(stream)
+            if any(mk[i][1] == 0 for i in undo):
+                su = set(undo)
+                state.write_markers([(t, 1 if i in su else u) for i, (t, u) in enumerate(mk)], stream)
+        opened: dict[bytes, C.c_void_p] = {}
+        first = True
+        for r in range(world):
+            if r == src:
+                continue
+            peer = {}
+            for n, (hb, off) in allh[r].items():
+                if hb not in opened:
+                    base = C.c_void_p()
+                    check(LIB.rw_ipc_import(hb, C.byref(base)))
+                    opened[hb] = base
+                peer[n] = C.c_void_p(opened[hb].value + off)
+            ids = undo if first else []  # later replacements receive the already-resolved state
+            arr = (C.c_uint32 * max(len(ids), 1))(*ids)
+            check(LIB.rw_undo_and_push(state.handle, C.byref(h), arr, len(ids), peer["x"], peer.get("g"),
+                                       peer.get("m"), peer.get("v"), sh))
+            first = False
+        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+        for base in opened.values():
+            check(LIB.rw_ipc_close(base))
+    dist.barrier(group=group)
+    mk = state.markers()
+    backend = dist.get_backend(group)
+    dev = state.device if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([v for pair in mk for v in pair], dtype=torch.int64, device=dev)
+    dist.broadcast(t, src=src, group=group)
+    flat = t.cpu().tolist()
+    state.write_markers([(flat[2 * i], flat[2 * i + 1]) for i in range(len(mk))])
+    return nbytes
+
+
 def recover_replication(state, src: int, include_grad: bool = False, group=None) -> int:
     """recover_replication: broadcast the resolved state from the
     surviving rank `src` to every other rank of `group` (NCCL over NVLink).

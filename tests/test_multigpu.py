@@ -1,0 +1,141 @@
+"""Multi-GPU recovery on the B200 box (needs >= 2 GPUs; skipped otherwise).
+
+* fused undo + NVLink push (rw_undo_and_push) == local undo, and the
+  replacement receives a bit-exact copy (copy semantics);
+* NCCL broadcast path gives the same bits;
+* parallel replay over 2 ranks (scatter + ordered merge + all-gather) ==
+  sequential replay bit for bit.
+"""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+needs2 = pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2,
+                            reason="needs 2 GPUs")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _run(fn, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    ps = [ctx.Process(target=_entry, args=(fn, r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return out
+
+
+def _entry(fn, rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        q.put((rank, fn(rank, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def scen_fused(rank, world):
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper, seeded_fill_
+    from paper_2302_06173_b200.recovery import (apply_resolution, recover_replication,
+                                                recover_replication_fused, resolve)
+    sizes = [100_003, 64, 5_000_017, 7, 1_234_567, 4096]
+    h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
+    st = DeviceState(sizes, kind=ADAM)
+    if rank == 0:
+        for i, t in enumerate((st.x, st.g, st.m, st.v)):
+            seeded_fill_(t, 40 + i)
+        st.v.abs_()
+        st.write_markers([(6, 0)] * len(sizes))
+        st.step(h, stop_after=3)                  # crash mid-update: groups 5,4,3 stepped
+        plan = resolve(st.markers(), h, lens=sizes)
+        # independent local resolution for comparison
+        twin = DeviceState(sizes, kind=ADAM)
+        for n in ("x", "g", "m", "v"):
+            getattr(twin, n).copy_(getattr(st, n))
+        twin.write_markers(st.markers())
+        apply_resolution(twin, h, plan)
+    else:
+        plan = resolve([], h)
+    nb = recover_replication_fused(st, h, plan, src=0)
+    res = {n: getattr(st, n).clone() for n in ("x", "m", "v")}
+    ok_local = True
+    if rank == 0:
+        ok_local = all(torch.equal(res[n].view(torch.int32), getattr(twin, n).view(torch.int32))
+                       for n in ("x", "m", "v"))
+    # bring rank 1's copy to rank 0 for comparison
+    same = []
+    for n in ("x", "m", "v"):
+        other = res[n].clone()
+        dist.broadcast(other, src=1)
+        same.append(torch.equal(other.view(torch.int32), res[n].view(torch.int32)))
+    # the NCCL path on the same state gives the same bits
+    st2 = DeviceState(sizes, kind=ADAM)
+    if rank == 0:
+        for n in ("x", "m", "v"):
+            getattr(st2, n).copy_(res[n])
+        st2.write_markers(st.markers())
+    recover_replication(st2, src=0)
+    same_nccl = all(torch.equal(getattr(st2, n).view(torch.int32), res[n].view(torch.int32))
+                    for n in ("x", "m", "v"))
+    return dict(strategy=plan.strategy, ok_local=ok_local, same=all(same), same_nccl=same_nccl,
+                markers=st.markers(), nbytes=nb)
+
+
+@needs2
+def test_fused_undo_push_bitexact():
+    out = _run(scen_fused)
+    assert out[0]["strategy"] == "Undo"
+    assert out[0]["ok_local"]
+    assert out[0]["same"] and out[1]["same"]
+    assert out[0]["same_nccl"] and out[1]["same_nccl"]
+    assert out[0]["markers"] == out[1]["markers"] == [(6, 0)] * 6
+
+
+def scen_parallel_replay(rank, world):
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import ADAM, OptimizerHyper
+    from paper_2302_06173_b200.replay import (BoundaryLog, Pipeline, Stage, recover_parallel,
+                                              replay_group)
+    h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
+    ghost = Pipeline(p=3, dim=64, hidden=128, layers=2, rows=128, micro_batches=4, seed=11, kind=ADAM, hyper=h)
+    log = BoundaryLog()
+    for it in range(3):
+        if it == 1:
+            snap = ghost.stages[1].snapshot()
+        ghost.run_iteration(log_group=(1, 1), log=log)
+    seq = Stage(1, 64, 128, 64, 2, 11, ADAM)
+    seq.restore(snap)
+    replay_group([seq], log, 1, 3, 128, 4, 11, h, first=False, last=False, dim=64)
+    par = Stage(1, 64, 128, 64, 2, 11, ADAM)
+    par.restore(snap)
+    recover_parallel([par], log, 1, 3, 128, 4, 11, h, first=False, last=False, dim=64, rank=rank, d=world)
+    return dict(eq_seq=all(torch.equal(getattr(par.state, n), getattr(seq.state, n)) for n in ("x", "m", "v")),
+                eq_ghost=torch.equal(par.state.x, ghost.stages[1].state.x))
+
+
+@needs2
+def test_parallel_replay_two_ranks_bitexact():
+    out = _run(scen_parallel_replay)
+    for r in (0, 1):
+        assert out[r]["eq_seq"] and out[r]["eq_ghost"]
