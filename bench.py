@@ -339,6 +339,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     modes = ["nccl", "fused"] if world > 1 else ["local"]
     for mode in modes:
         res = []
+        kinfo = []
         for it in range(steps + 1):
             if rank == 0:
                 st.write_markers([(10, 0)] * st.num_groups)
@@ -351,6 +352,9 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
                            device=device)
             if mode == "fused":
                 nbytes = recover_replication_fused(st, h, plan, src=0)
+                if rank == 0:
+                    from paper_2302_06173_b200 import recovery as _rec
+                    kinfo.append(dict(_rec.LAST_FUSED_INFO))
             else:
                 if rank == 0:
                     apply_resolution(st, h, plan)
@@ -368,6 +372,11 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
                          bytes_per_replacement=nbytes,
                          transfer_algbw_gbs=round(nbytes / (ms * 1e-3) / 1e9, 1) if nbytes else None,
                          frac_of_nvlink_roofline=round(nbytes / 770e9 / (ms * 1e-3), 3) if nbytes else None)
+        if kinfo:
+            km = statistics.median(k["kernel_ms"] for k in kinfo[1:] or kinfo)
+            out[mode]["push_kernel_ms"] = round(km, 3)
+            out[mode]["push_kernel_gbs"] = round(nbytes / (km * 1e-3) / 1e9, 1)
+            out[mode]["ipc_map_ms_first"] = round(kinfo[0]["map_ms"], 3)
     del st
     torch.cuda.empty_cache()
     out["workload"] = ("config 3: GPT-2 XL (1,557,611,200 params, 580 groups) Adam fp32; rank 0 crashed "

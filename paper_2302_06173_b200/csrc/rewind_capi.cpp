@@ -184,6 +184,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     for (auto& kv : set_of) kv.second = k++;
   }
   for (uint32_t i = 0; i < n; ++i) {
+    if (copy_only && copy_only[i]) continue;  // pass-through groups use no scalars
     const rw_group& gr = s->mirror[ids[i]];
     const uint64_t tt = undo ? gr.t : gr.t + 1;
     sl.h_sets[set_of[tt]] = scalars_at(h, tt, etas[i]);

@@ -14,6 +14,7 @@ logic.  The per-group decisions are made by the C++ resolver
 from __future__ import annotations
 
 import ctypes as C
+import time
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -56,7 +57,10 @@ def _allreduce_u64(vals: list[int], op, group=None, device=None) -> list[int]:
     if not (dist.is_available() and dist.is_initialized()):
         return list(vals)
     backend = dist.get_backend(group)
-    dev = device if backend == "nccl" else torch.device("cpu")
+    if backend == "nccl":
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    else:
+        dev = torch.device("cpu")
     t = torch.tensor([int(v) for v in vals], dtype=torch.int64, device=dev)
     dist.all_reduce(t, op=op, group=group)
     return [int(v) for v in t.cpu().tolist()]
@@ -126,6 +130,16 @@ def apply_resolution(state, hyper, plan: ResolvePlan, grad: torch.Tensor | None 
         state.step(hyper, order, grad=grad, stream=stream)
 
 
+_PEER_MAPS: dict[bytes, C.c_void_p] = {}  # IPC handle -> mapped base (kept for reuse)
+LAST_FUSED_INFO: dict = {}
+
+
+def release_peer_mappings() -> None:
+    for base in _PEER_MAPS.values():
+        LIB.rw_ipc_close(base)
+    _PEER_MAPS.clear()
+
+
 def _export(t: torch.Tensor) -> tuple[bytes, int]:
     h = (C.c_uint8 * 64)()
     off = C.c_uint64()
@@ -158,26 +172,34 @@ def recover_replication_fused(state, hyper, plan: ResolvePlan, src: int, include
             if any(mk[i][1] == 0 for i in undo):
                 su = set(undo)
                 state.write_markers([(t, 1 if i in su else u) for i, (t, u) in enumerate(mk)], stream)
-        opened: dict[bytes, C.c_void_p] = {}
+        t0 = time.perf_counter()
         first = True
+        peers = []
         for r in range(world):
             if r == src:
                 continue
             peer = {}
             for n, (hb, off) in allh[r].items():
-                if hb not in opened:
+                if hb not in _PEER_MAPS:  # map each replacement allocation once
                     base = C.c_void_p()
                     check(LIB.rw_ipc_import(hb, C.byref(base)))
-                    opened[hb] = base
-                peer[n] = C.c_void_p(opened[hb].value + off)
+                    _PEER_MAPS[hb] = base
+                peer[n] = C.c_void_p(_PEER_MAPS[hb].value + off)
+            peers.append(peer)
+        t1 = time.perf_counter()
+        cs = stream or torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        for peer in peers:
             ids = undo if first else []  # later replacements receive the already-resolved state
             arr = (C.c_uint32 * max(len(ids), 1))(*ids)
             check(LIB.rw_undo_and_push(state.handle, C.byref(h), arr, len(ids), peer["x"], peer.get("g"),
                                        peer.get("m"), peer.get("v"), sh))
             first = False
-        torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
-        for base in opened.values():
-            check(LIB.rw_ipc_close(base))
+        e1.record(cs)
+        cs.synchronize()
+        LAST_FUSED_INFO.clear()
+        LAST_FUSED_INFO.update(map_ms=(t1 - t0) * 1e3, kernel_ms=e0.elapsed_time(e1))
     dist.barrier(group=group)
     mk = state.markers()
     backend = dist.get_backend(group)

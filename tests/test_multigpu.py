@@ -83,11 +83,13 @@ def scen_fused(rank, world):
         ok_local = all(torch.equal(res[n].view(torch.int32), getattr(twin, n).view(torch.int32))
                        for n in ("x", "m", "v"))
     # bring rank 1's copy to rank 0 for comparison
+    # (group contents only: the push moves every group; inter-group padding is not state)
     same = []
     for n in ("x", "m", "v"):
         other = res[n].clone()
         dist.broadcast(other, src=1)
-        same.append(torch.equal(other.view(torch.int32), res[n].view(torch.int32)))
+        same.append(all(torch.equal(other[o:o + k].view(torch.int32), res[n][o:o + k].view(torch.int32))
+                        for o, k in zip(st.offsets, st.sizes)))
     # the NCCL path on the same state gives the same bits
     st2 = DeviceState(sizes, kind=ADAM)
     if rank == 0:
@@ -95,15 +97,22 @@ def scen_fused(rank, world):
             getattr(st2, n).copy_(res[n])
         st2.write_markers(st.markers())
     recover_replication(st2, src=0)
-    same_nccl = all(torch.equal(getattr(st2, n).view(torch.int32), res[n].view(torch.int32))
-                    for n in ("x", "m", "v"))
-    return dict(strategy=plan.strategy, ok_local=ok_local, same=all(same), same_nccl=same_nccl,
-                markers=st.markers(), nbytes=nb)
+    same_nccl = all(torch.equal(getattr(st2, n)[o:o + k].view(torch.int32), res[n][o:o + k].view(torch.int32))
+                    for n in ("x", "m", "v") for o, k in zip(st.offsets, st.sizes))
+    diffs = {}
+    if rank == 0:
+        for n in ("x", "m", "v"):
+            d = (res[n] - getattr(twin, n)).abs()
+            bad = torch.nonzero(res[n].view(torch.int32) != getattr(twin, n).view(torch.int32))
+            diffs[n] = (float(d.max()), int(bad.numel()), bad[:5].flatten().tolist())
+    return dict(strategy=plan.strategy, ok_local=ok_local, same=all(same), same_list=same,
+                same_nccl=same_nccl, markers=st.markers(), nbytes=nb, diffs=diffs)
 
 
 @needs2
 def test_fused_undo_push_bitexact():
     out = _run(scen_fused)
+    print(out[0]["diffs"], out[0]["same_list"], out[1]["same_list"], out[0]["same_nccl"], out[0]["markers"])
     assert out[0]["strategy"] == "Undo"
     assert out[0]["ok_local"]
     assert out[0]["same"] and out[1]["same"]
