@@ -158,6 +158,120 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n, int a_major, int
          | (uint32_t(m >> 4) << 24);    // M / 16
 }
 
+// Epilogue of one 32-column TMEM chunk for one accumulator row (thread).
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int N, const EpiArgs& ep) {
+    if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
+      float* o = static_cast<float*>(ep.out) + int64_t(row) * ep.ldo + col0;
+      if (col0 + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 w = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          if constexpr (EPI == EPI_F32_ACC) {
+            const float4 p = *reinterpret_cast<const float4*>(o + j);
+            w.x = __fadd_rn(p.x, w.x);
+            w.y = __fadd_rn(p.y, w.y);
+            w.z = __fadd_rn(p.z, w.z);
+            w.w = __fadd_rn(p.w, w.w);
+          }
+          *reinterpret_cast<float4*>(o + j) = w;
+        }
+      } else {
+        for (int j = 0; j < 32 && col0 + j < N; ++j)
+          o[j] = EPI == EPI_F32_ACC ? __fadd_rn(o[j], v[j]) : v[j];
+      }
+    } else {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + int64_t(row) * ep.ldo + col0;
+      const bool full = col0 + 32 <= N;
+      float w[32];
+      if constexpr (EPI == EPI_BIAS_TANH_BF16) {
+        float bv[32];
+        if (full) {  // same 128 B for every lane of the warp: one broadcast transaction each
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 b4 = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j));
+            bv[j] = b4.x;
+            bv[j + 1] = b4.y;
+            bv[j + 2] = b4.z;
+            bv[j + 3] = b4.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bv[j] = (col0 + j < N) ? __ldg(ep.bias + col0 + j) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = tanhf(__fadd_rn(v[j], bv[j]));
+      } else if constexpr (EPI == EPI_DTANH_BF16) {
+        const __nv_bfloat16* yp = ep.y + int64_t(row) * ep.ldy + col0;
+        float yv[32];
+        if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            const uint4 u = *reinterpret_cast<const uint4*>(yp + j);
+            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 f = __bfloat1622float2(p2[q]);
+              yv[j + 2 * q] = f.x;
+              yv[j + 2 * q + 1] = f.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) yv[j] = (col0 + j < N) ? __bfloat162float(yp[j]) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = __fmul_rn(v[j], __fsub_rn(1.f, __fmul_rn(yv[j], yv[j])));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = v[j];
+      }
+      if (col0 + 32 <= N) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          uint4 pk;
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(w[j], w[j + 1]);
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(w[j + 2], w[j + 3]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(w[j + 4], w[j + 5]);
+          __nv_bfloat162 h3 = __floats2bfloat162_rn(w[j + 6], w[j + 7]);
+          pk.x = *reinterpret_cast<uint32_t*>(&h0);
+          pk.y = *reinterpret_cast<uint32_t*>(&h1);
+          pk.z = *reinterpret_cast<uint32_t*>(&h2);
+          pk.w = *reinterpret_cast<uint32_t*>(&h3);
+          *reinterpret_cast<uint4*>(o + j) = pk;
+        }
+      } else {
+        for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(w[j]);
+      }
+    }
+}
+
+// Drain one accumulator tile: this thread owns TMEM lane `row - m0`.
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, int n0, int M, int N, const EpiArgs& ep) {
+#pragma unroll 1
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    float v[32];
+    tmem_ld_32cols(tbase + uint32_t(c0), v);
+    if (row < M) epi_chunk<EPI>(v, row, n0 + c0, N, ep);
+  }
+}
+
+// Grouped tile rasterization: consecutive tile ids walk GM M-tiles down one
+// N column before moving right, so the ~148 concurrently active tiles cover a
+// compact GM x (148/GM) block whose A and B panels stay resident in the
+// 126 MB L2 (plain M-fastest order re-streams the whole A panel per N tile).
+__device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int gm, int& tm, int& tn) {
+  const int per_group = gm * tiles_n;
+  const int group = tile / per_group;
+  const int first_m = group * gm;
+  const int gsz = min(tiles_m - first_m, gm);
+  const int in = tile - group * per_group;
+  tm = first_m + in % gsz;
+  tn = in / gsz;
+}
+constexpr int kGroupM = 16;
+
 template <int BN>
 struct Cfg {
   static constexpr int kStages = BN == 256 ? 4 : 6;
@@ -219,7 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int tm = tile % tiles_m, tn = tile / tiles_m;  // M-fastest: B tile reused via L2
+        int tm, tn;
+        tile_coords(tile, tiles_m, tiles_n, kGroupM, tm, tn);
         const int m0 = tm * BM, n0 = tn * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -296,103 +411,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int tm = tile % tiles_m, tn = tile / tiles_m;
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, kGroupM, tm, tn);
       const int m0 = tm * BM, n0 = tn * BN;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const int row = m0 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld_32cols(tbase + uint32_t(c0), v);
-        const int col0 = n0 + c0;
-        if (row < M) {
-          if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
-            float* o = static_cast<float*>(ep.out) + int64_t(row) * ep.ldo + col0;
-            if (col0 + 32 <= N) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 4) {
-                float4 w = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                if constexpr (EPI == EPI_F32_ACC) {
-                  const float4 p = *reinterpret_cast<const float4*>(o + j);
-                  w.x = __fadd_rn(p.x, w.x);
-                  w.y = __fadd_rn(p.y, w.y);
-                  w.z = __fadd_rn(p.z, w.z);
-                  w.w = __fadd_rn(p.w, w.w);
-                }
-                *reinterpret_cast<float4*>(o + j) = w;
-              }
-            } else {
-              for (int j = 0; j < 32 && col0 + j < N; ++j)
-                o[j] = EPI == EPI_F32_ACC ? __fadd_rn(o[j], v[j]) : v[j];
-            }
-          } else {
-            __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + int64_t(row) * ep.ldo + col0;
-            const bool full = col0 + 32 <= N;
-            float w[32];
-            if constexpr (EPI == EPI_BIAS_TANH_BF16) {
-              float bv[32];
-              if (full) {  // same 128 B for every lane of the warp: one broadcast transaction each
-#pragma unroll
-                for (int j = 0; j < 32; j += 4) {
-                  const float4 b4 = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j));
-                  bv[j] = b4.x;
-                  bv[j + 1] = b4.y;
-                  bv[j + 2] = b4.z;
-                  bv[j + 3] = b4.w;
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) bv[j] = (col0 + j < N) ? __ldg(ep.bias + col0 + j) : 0.f;
-              }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) w[j] = tanhf(__fadd_rn(v[j], bv[j]));
-            } else if constexpr (EPI == EPI_DTANH_BF16) {
-              const __nv_bfloat16* yp = ep.y + int64_t(row) * ep.ldy + col0;
-              float yv[32];
-              if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads
-#pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                  const uint4 u = *reinterpret_cast<const uint4*>(yp + j);
-                  const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                  for (int q = 0; q < 4; ++q) {
-                    const float2 f = __bfloat1622float2(p2[q]);
-                    yv[j + 2 * q] = f.x;
-                    yv[j + 2 * q + 1] = f.y;
-                  }
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) yv[j] = (col0 + j < N) ? __bfloat162float(yp[j]) : 0.f;
-              }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) w[j] = __fmul_rn(v[j], __fsub_rn(1.f, __fmul_rn(yv[j], yv[j])));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j) w[j] = v[j];
-            }
-            if (col0 + 32 <= N) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                uint4 pk;
-                __nv_bfloat162 h0 = __floats2bfloat162_rn(w[j], w[j + 1]);
-                __nv_bfloat162 h1 = __floats2bfloat162_rn(w[j + 2], w[j + 3]);
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(w[j + 4], w[j + 5]);
-                __nv_bfloat162 h3 = __floats2bfloat162_rn(w[j + 6], w[j + 7]);
-                pk.x = *reinterpret_cast<uint32_t*>(&h0);
-                pk.y = *reinterpret_cast<uint32_t*>(&h1);
-                pk.z = *reinterpret_cast<uint32_t*>(&h2);
-                pk.w = *reinterpret_cast<uint32_t*>(&h3);
-                *reinterpret_cast<uint4*>(o + j) = pk;
-              }
-            } else {
-              for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(w[j]);
-            }
-          }
-        }
-      }
+      epilogue_tile<BN, EPI>(tbase, row, n0, M, N, ep);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -407,6 +433,227 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(C::kTmemCols));
+  }
+}
+
+// ===================================================================================
+// CTA-pair variant: tcgen05.mma.cta_group::2 with M = 256 per pair.  Each CTA
+// of a (2,1,1) cluster loads its own 128 rows of A and HALF of the B tile
+// (BN/2 rows) into the same smem offsets; the leader (rank 0) issues the MMAs
+// for both, each CTA's TMEM receives its 128 accumulator rows.  Per SM the
+// tensor core now reads 128x16 of A + (BN/2)x16 of B per instruction instead
+// of 128x16 + BNx16, which relieves the shared-memory bandwidth that limits
+// the single-CTA kernel.
+// ===================================================================================
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t local_smem_addr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local_smem_addr));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA load into this CTA's smem, completion counted on the LEADER's barrier
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// arrive (once the issued MMAs complete) on the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+template <int BN>
+struct Cfg2 {
+  static constexpr int BNH = BN / 2;
+  static constexpr int kStages = 6;
+  static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB: this CTA's 128 rows
+  static constexpr uint32_t kBBytes = BNH * BK * 2;  // 16 KB: half of the B tile
+  static constexpr uint32_t kStageBytes = kABytes + kBBytes;
+  static constexpr uint32_t kTmemCols = 2 * BN;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024;
+};
+
+template <int BN, int AMAJ, int BMAJ, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    umma_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                      int M, int N, int K, EpiArgs ep) {
+  using C = Cfg2<BN>;
+  constexpr int S = C::kStages;
+  constexpr int BNH = C::BNH;
+  constexpr int PM = 2 * BM;  // rows per CTA pair
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int tiles_m = (M + PM - 1) / PM, tiles_n = (N + BN - 1) / BN;
+  const int num_tiles = tiles_m * tiles_n;
+  const int num_kb = (K + BK - 1) / BK;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&tma_a);
+    prefetch_tmap(&tma_b);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 2);  // leader: its expect_tx arrive + the peer's arrive
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base_sh)),
+                 "r"(C::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = tmem_base_sh;
+
+  if (warp == 0) {
+    // ===================== TMA producer (both CTAs) =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
+        const int m0 = tm * PM + int(rank) * BM;     // this CTA's A rows
+        const int nb0 = tn * BN + int(rank) * BNH;   // this CTA's half of B
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kABytes;
+          const uint32_t fb = smem_u32(&full_bar[stage]);
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
+          else mbar_arrive_cluster(mapa_rank0(fb));
+          const uint32_t lbar = fb & 0xFEFFFFFFu;  // the leader's barrier
+          const int k0 = kb * BK;
+          if constexpr (AMAJ == K_MAJOR) {
+            tma_load_2d_2sm(sa, &tma_a, lbar, k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d_2sm(sa + c * kMnChunkBytes, &tma_a, lbar, m0 + c * 64, k0);
+          }
+          if constexpr (BMAJ == K_MAJOR) {
+            tma_load_2d_2sm(sb, &tma_b, lbar, k0, nb0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BNH / 64; ++c) tma_load_2d_2sm(sb + c * kMnChunkBytes, &tma_b, lbar, nb0 + c * 64, k0);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer (leader CTA only) =====================
+    if (leader) {
+      constexpr uint32_t idesc = make_idesc(PM, BN, AMAJ, BMAJ);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = cid; tile < num_tiles; tile += ncl) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
+            const uint32_t sb = sa + C::kABytes;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = AMAJ == K_MAJOR ? make_desc(sa + k * 32, 16, 1024)
+                                                  : make_desc(sa + k * 2048, kMnChunkBytes, 1024);
+              const uint64_t bd = BMAJ == K_MAJOR ? make_desc(sb + k * 32, 16, 1024)
+                                                  : make_desc(sb + k * 2048, kMnChunkBytes, 1024);
+              tc_mma2(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            tc_commit2_mc(&empty_bar[stage]);  // frees this stage in BOTH CTAs
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (lane == 0) tc_commit2_mc(&tfull_bar[acc]);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ===================== epilogue (both CTAs, own 128 rows) =====================
+    const int ew = warp - kEpiWarp0;
+    const uint32_t tempty_leader = mapa_rank0(smem_u32(&tempty_bar[0]));
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cid; tile < num_tiles; tile += ncl) {
+      int tm, tn;
+      tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const int row = tm * PM + int(rank) * BM + ew * 32 + lane;
+      const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
+      epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(C::kTmemCols));
   }
 }
 

@@ -72,5 +72,33 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
   return static_cast<int>(cudaGetLastError());
 }
 
+// CTA-pair (cta_group::2) variant: same contract, M tiles of 256 per pair.
+template <int BN, int AMAJ, int BMAJ, int EPI>
+int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
+            cudaStream_t stream, int max_ctas = 0) {
+  CUtensorMap ma, mb;
+  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM) : make_map(&ma, A, K, M, lda, 64);
+  if (e) return e;
+  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN / 2) : make_map(&mb, B, K, N, ldb, 64);
+  if (e) return e;
+  auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(Cfg2<BN>::kSmem));
+    if (ce != cudaSuccess) return static_cast<int>(ce);
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  int pairs = sms / 2;
+  if (tiles < pairs) pairs = tiles;
+  if (max_ctas > 0 && pairs * 2 > max_ctas) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
+  kern<<<pairs * 2, kThreads, Cfg2<BN>::kSmem, stream>>>(ma, mb, M, N, K, ep);
+  return static_cast<int>(cudaGetLastError());
+}
+
 }  // namespace gemm
 }  // namespace rwb

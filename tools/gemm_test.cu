@@ -24,6 +24,13 @@ using namespace rwb::gemm;
     }                                                                          \
   } while (0)
 
+template <int BN, int AM, int BMJ, int EPI, bool PAIR>
+int run_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
+             cudaStream_t s) {
+  if constexpr (PAIR) return launch2<BN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, s);
+  else return launch<BN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, s);
+}
+
 __global__ void fill_bf16(__nv_bfloat16* p, size_t n, uint32_t seed, float scale) {
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
     uint32_t h = uint32_t(i) * 2654435761u ^ seed;
@@ -48,7 +55,7 @@ __global__ void ref_gemm(const __nv_bfloat16* A, int64_t lda, int amaj, const __
   C[int64_t(m) * N + n] = acc;
 }
 
-template <int BN, int AM, int BMJ, int EPI>
+template <int BN, int AM, int BMJ, int EPI, bool PAIR = false>
 bool check(const char* name, int M, int N, int K) {
   size_t na = size_t(M) * K, nb = size_t(N) * K;
   __nv_bfloat16 *A, *B, *Y, *O;
@@ -78,13 +85,13 @@ bool check(const char* name, int M, int N, int K) {
   } else {
     ep.out = O;
   }
-  int e = launch<BN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, 0);
+  int e = run_gemm<BN, AM, BMJ, EPI, PAIR>(A, lda, B, ldb, M, N, K, ep, 0);
   if (e) {
     printf("%s: launch error %d\n", name, e);
     return false;
   }
   if (EPI == EPI_F32_ACC) {  // second pass accumulates: result = 2 * C
-    e = launch<BN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, 0);
+    e = run_gemm<BN, AM, BMJ, EPI, PAIR>(A, lda, B, ldb, M, N, K, ep, 0);
   }
   CK(cudaDeviceSynchronize());
   dim3 g((N + 127) / 128, M);
@@ -128,7 +135,7 @@ bool check(const char* name, int M, int N, int K) {
   return ok;
 }
 
-template <int BN, int AM, int BMJ, int EPI>
+template <int BN, int AM, int BMJ, int EPI, bool PAIR = false>
 void perf(const char* name, int M, int N, int K, int reps = 10) {
   __nv_bfloat16 *A, *B, *O;
   float* bias;
@@ -149,12 +156,12 @@ void perf(const char* name, int M, int N, int K, int reps = 10) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  launch<BN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, 0);
+  run_gemm<BN, AM, BMJ, EPI, PAIR>(A, lda, B, ldb, M, N, K, ep, 0);
   CK(cudaDeviceSynchronize());
   float best = 1e30f;
   for (int r = 0; r < reps; ++r) {
     CK(cudaEventRecord(e0));
-    launch<BN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, 0);
+    run_gemm<BN, AM, BMJ, EPI, PAIR>(A, lda, B, ldb, M, N, K, ep, 0);
     CK(cudaEventRecord(e1));
     CK(cudaEventSynchronize(e1));
     float ms;
@@ -181,12 +188,28 @@ int main(int argc, char** argv) {
   all &= check<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16>("dgrad *(1-y^2) bf16", 384, 512, 768);
   all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32_ACC>("wgrad f32 accumulate", 512, 256, 1024);
   all &= check<256, K_MAJOR, K_MAJOR, EPI_BF16>("KK bf16 big", 2048, 2048, 2048);
+  // CTA-pair (cta_group::2) kernel
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_F32, true>("PAIR KK f32", 512, 512, 256);
+  all &= check<256, K_MAJOR, MN_MAJOR, EPI_F32, true>("PAIR K/MN f32", 512, 512, 256);
+  all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32, true>("PAIR MN/MN f32", 512, 512, 256);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_F32, true>("PAIR KK f32 ragged", 300, 300, 136);
+  all &= check<256, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16, true>("PAIR forward bias+tanh", 512, 768, 512);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16, true>("PAIR dgrad dtanh", 512, 512, 768);
+  all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32_ACC, true>("PAIR wgrad accumulate", 512, 256, 1024);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_BF16, true>("PAIR KK bf16 big", 2048, 2048, 2048);
   printf("correctness: %s\n", all ? "ALL OK" : "FAILURES");
   if (argc > 1) {
     perf<256, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward 16384x16384x4096", 16384, 16384, 4096);
     perf<256, K_MAJOR, K_MAJOR, EPI_BF16>("dgrad 16384x4096x16384", 16384, 4096, 16384);
     perf<256, MN_MAJOR, MN_MAJOR, EPI_F32>("wgrad 4096x16384x16384", 4096, 16384, 16384);
     perf<256, K_MAJOR, K_MAJOR, EPI_BF16>("KK 8192^3", 8192, 8192, 8192);
+    perf<256, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16, true>("PAIR forward 16384x16384x4096", 16384, 16384, 4096);
+    perf<256, K_MAJOR, K_MAJOR, EPI_BF16, true>("PAIR dgrad 16384x4096x16384", 16384, 4096, 16384);
+    perf<256, MN_MAJOR, MN_MAJOR, EPI_F32, true>("PAIR wgrad 4096x16384x16384", 4096, 16384, 16384);
+    perf<256, K_MAJOR, K_MAJOR, EPI_BF16, true>("PAIR KK 8192^3", 8192, 8192, 8192);
+    perf<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16, true>("PAIR dgrad-dtanh 16384x16384x4096", 16384, 16384, 4096);
+    perf<128, K_MAJOR, K_MAJOR, EPI_BF16, true>("PAIR BN128 KK 8192^3", 8192, 8192, 8192);
+    perf<128, K_MAJOR, K_MAJOR, EPI_BF16, false>("BN128 KK 8192^3", 8192, 8192, 8192);
   }
   return all ? 0 : 1;
 }
