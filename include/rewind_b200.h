@@ -259,6 +259,51 @@ int rw_mse_grad(const void* pred_bf16, const float* target, uint64_t n, uint64_t
 /* fp32 -> bf16 (weight shadows after an optimizer step) */
 int rw_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream);
 
+/* ---- logging capture path (logstore.cpp missing) ----
+ * Upstream-backup log of inter-machine boundary tensors.  rw_logger_log never
+ * blocks the producer stream: it orders a CRC32 kernel and a D2H copy into a
+ * pinned slab on the logger's own stream (the paper's dedicated copy
+ * stream), and pushes the record onto a single-producer/single-consumer
+ * queue; a native committer thread waits for the copy event and appends the
+ * record to the current chunk file.  Chunk files hold `chunk_records`
+ * records: "SWFT" | u16 version | u32 machine, then length-prefixed
+ * little-endian records (header, payload, CRC32 of the payload), written to
+ * a .tmp name and renamed into place when complete (atomic commit). */
+enum { RW_LOG_ACTIVATION = 0, RW_LOG_GRADIENT = 1 };
+typedef struct rw_log_record {
+  uint32_t sender;          /* LogRecord fields */
+  uint32_t receiver;
+  uint64_t iteration;
+  uint32_t mb;
+  uint32_t direction;       /* RW_LOG_ACTIVATION / RW_LOG_GRADIENT */
+  uint32_t dtype;           /* RW_F32 / RW_F64 / RW_BF16 */
+  uint32_t ndim;            /* <= 4 */
+  uint64_t shape[4];
+  uint64_t payload_bytes;
+  uint32_t crc32;           /* CRC32 of the payload (wire.cpp:31-38) */
+  uint32_t _pad;
+} rw_log_record;
+
+/* CRC32 of a device buffer, written to *out_dev (device memory). */
+int rw_crc32_device(const void* data, uint64_t n, uint32_t* out_dev, void* stream);
+
+typedef struct rw_logger rw_logger;
+int rw_logger_create(rw_logger** out, const char* dir, uint32_t machine, uint32_t chunk_records,
+                     uint64_t pinned_bytes, int32_t device);
+/* log_send: rec's shape/ids/dtype; payload_bytes = bytes of dev_payload. */
+int rw_logger_log(rw_logger* lg, const rw_log_record* rec, const void* dev_payload, void* producer_stream);
+/* flush_logs: drain the queue, commit the partial chunk. */
+int rw_logger_flush(rw_logger* lg, uint64_t* records_committed);
+int rw_logger_destroy(rw_logger* lg);
+
+typedef struct rw_log_reader rw_log_reader;
+int rw_log_open(rw_log_reader** out, const char* path, uint32_t* machine);
+/* next record header + payload into `payload` (cap bytes); *eof = 1 at end.
+ * RW_CORRUPT_LOG on a malformed file.  The payload CRC is checked by the
+ * caller on the device (rw_crc32_device) against rec->crc32. */
+int rw_log_next(rw_log_reader* r, rw_log_record* rec, void* payload, uint64_t cap, int32_t* eof);
+void rw_log_close(rw_log_reader* r);
+
 /* ---- selective-logging policy (planner.cpp missing) ---- */
 /* bubble_ratio(p, m), schedule.cpp:86-93 */
 int rw_bubble_ratio(int32_t p, int32_t m, int64_t* num, int64_t* den);

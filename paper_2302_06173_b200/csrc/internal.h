@@ -70,6 +70,11 @@ int launch_ordered_sum(int dtype, const void* const* tensors, uint32_t count, ui
                        void* stream);
 int launch_clear_updated(rw_group* groups, const uint32_t* ids, uint32_t n, void* stream);
 
+// log_kernels.cu: CRC32 (wire.cpp:31-38) of a device buffer into *out_dev;
+// scratch = crc32_scratch_words(n) device uint32 words
+int launch_crc32(const void* data, uint64_t n, uint32_t* out_dev, uint32_t* scratch, void* stream);
+uint64_t crc32_scratch_words(uint64_t n);
+
 // replay_kernels.cu (all return cudaError_t as int)
 int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, const void* w, const float* b,
                          void* y, void* stream);

@@ -211,7 +211,7 @@ class BoundaryLog:
     grads: dict = field(default_factory=dict)
     pinned: bool = False
 
-    def put(self, kind: str, it: int, mb: int, t: torch.Tensor) -> None:
+    def put(self, kind: str, it: int, mb: int, t: torch.Tensor, sender: int = 0, receiver: int = 0) -> None:
         if self.pinned:
             h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
             h.copy_(t, non_blocking=True)
@@ -231,6 +231,17 @@ class BoundaryLog:
         return sum(t.numel() * t.element_size() for d in (self.acts, self.grads) for t in d.values())
 
 
+class _LoggerSink:
+    """Adapts logstore.Logger to the BoundaryLog.put interface (machine = stage)."""
+
+    def __init__(self, logger):
+        self.lg = logger
+
+    def put(self, kind: str, it: int, mb: int, t: torch.Tensor, sender: int = 0, receiver: int = 0) -> None:
+        from .logstore import RW_LOG_ACTIVATION, RW_LOG_GRADIENT
+        self.lg.log_send(t, sender, receiver, it, mb, RW_LOG_ACTIVATION if kind == "act" else RW_LOG_GRADIENT)
+
+
 class Pipeline:
     """A p-stage pipeline on one GPU used as the failure-free "ghost run"
     (SPEC:510): same seeds, same kernels.  Logs the boundaries around a group of
@@ -243,7 +254,15 @@ class Pipeline:
         self.iteration = 0
         self.losses: list[float] = []
 
-    def run_iteration(self, log_group: tuple[int, int] | None = None, log: BoundaryLog | None = None) -> float:
+    def run_iteration(self, log_group: tuple[int, int] | None = None, log=None) -> float:
+        """One training iteration.  `log` is a BoundaryLog (in HBM / pinned) or a
+        logstore.Logger (async D2H + SWFT chunk files); the messages into the
+        group [g0, g1] are logged at send time (upstream backup)."""
+        if log is not None and not isinstance(log, BoundaryLog):
+            return self._run_iteration(log_group, _LoggerSink(log))
+        return self._run_iteration(log_group, log)
+
+    def _run_iteration(self, log_group, log) -> float:
         it = self.iteration
         dev = self.stages[0].device
         loss = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -255,7 +274,7 @@ class Pipeline:
                 acts = st.new_acts(self.rows)
                 acts[0].copy_(x)
                 if log_group and log is not None and s == log_group[0] and s > 0:
-                    log.put("act", it, mb, x)
+                    log.put("act", it, mb, x, sender=s - 1, receiver=s)
                 x = st.forward(acts)
                 all_acts.append(acts)
             tgt = synth_targets(self.seed, it, mb, self.rows, self.dim, device=dev)
@@ -263,7 +282,7 @@ class Pipeline:
             tot += float(loss.item())
             for s in range(self.p - 1, -1, -1):
                 if log_group and log is not None and s == log_group[1] and s < self.p - 1:
-                    log.put("grad", it, mb, g)
+                    log.put("grad", it, mb, g, sender=s + 1, receiver=s)
                 gout = torch.empty(self.rows, self.dim, dtype=torch.bfloat16, device=dev) if s > 0 else None
                 self.stages[s].backward(all_acts[s], g, gout, accumulate=mb > 0)
                 g = gout
