@@ -114,7 +114,9 @@ def read_chunk(path: str, max_payload: int = 1 << 30) -> Iterator[tuple[rw_log_r
     m = _u32()
     check(LIB.rw_log_open(C.byref(h), path.encode(), C.byref(m)))
     try:
-        buf = torch.empty(max(max_payload, 1), dtype=torch.uint8, pin_memory=True)
+        # pinned when a device is present (fast H2D for replay); the reader itself is host code
+        cap = max(1, min(max_payload, os.path.getsize(path)))  # a record never exceeds its file
+        buf = torch.empty(cap, dtype=torch.uint8, pin_memory=torch.cuda.is_available())
         while True:
             r = rw_log_record()
             eof = C.c_int32()
