@@ -137,6 +137,18 @@ int rw_clear_updated(rw_state* s, const uint32_t* group_ids, uint32_t n, void* s
 /* Device pointers of the flat buffers (for collectives / copies). */
 void* rw_state_ptr(rw_state* s, int which /*0 x,1 g,2 m,3 v,4 vmax*/);
 
+/* LAMB saved scalars (ParamBlock::saved_scalars, optim.hpp / optim.cpp:294,
+ * :319).  Each group keeps the last RW_LAMB_TRUST_DEPTH trust ratios on the
+ * device (a step pushes, an undo pops; older entries fall off, so at most
+ * RW_LAMB_TRUST_DEPTH consecutive undos find their ratio).  read copies the
+ * stack bottom->top into out (at most cap) and its depth into *count
+ * (synchronises `stream`); write replaces it (count <= RW_LAMB_TRUST_DEPTH),
+ * e.g. on a replacement receiving a survivor's state. */
+#define RW_LAMB_TRUST_DEPTH 8
+int rw_state_saved_scalars(rw_state* s, uint32_t group, double* out, uint32_t cap, uint32_t* count,
+                           void* stream);
+int rw_state_set_saved_scalars(rw_state* s, uint32_t group, const double* in, uint32_t count, void* stream);
+
 /* optimizer_step(ParamBlock&, const Tensor& grad, const OptimizerHyper&),
  * optim.hpp:71-72 / optim.cpp:338-364 — batched over `n` groups given in
  * UPDATE ORDER (apply_layerwise_updates: reverse layer order).
@@ -149,7 +161,12 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* group_ids,
                       const void* grad, uint32_t stop_after, void* stream);
 
 /* optimizer_undo(ParamBlock&, const OptimizerHyper&), optim.hpp:76 /
- * optim.cpp:366-385 — batched over `n` groups. */
+ * optim.cpp:366-385 — batched over `n` groups.
+ * LAMB (step and undo): the step runs a per-group norm pass (m, v, ||x||,
+ * ||update|| in fp64 with a fixed reduction order) and then the fused x pass
+ * with scaled = eta * trust; the undo reads the saved ratio (one D2H read) and
+ * is one fused elementwise pass.  The trust ratio differs from the reference's
+ * sequential sum in the last bits (documented tolerance); m, v are bit-exact. */
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
                       void* stream);
 
@@ -180,6 +197,14 @@ int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* 
                        uint64_t* t, uint32_t* updated, const void* grad, const rw_hyper* h);
 int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n,
                        uint64_t* t, uint32_t* updated, const rw_hyper* h);
+/* LAMB on a host ParamBlock: the block's saved_scalars stack stays with the
+ * caller.  step returns the ratio step_lamb pushes (optim.cpp:294) in
+ * *trust_out; undo takes the stack top (the caller pops it on RW_OK, :319).
+ * rw_host_block_step/undo refuse RW_LAMB (they have no saved-scalar slot). */
+int rw_host_block_lamb_step(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
+                            uint32_t* updated, const void* grad, const rw_hyper* h, double* trust_out);
+int rw_host_block_lamb_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
+                            uint32_t* updated, const rw_hyper* h, uint32_t have_saved, double trust);
 
 /* ---- consistency resolver (no reference source) ---- */
 enum { RW_ACT_NONE = 0, RW_ACT_UNDO = 1, RW_ACT_REDO = 2 };

@@ -132,6 +132,16 @@ void optimizer_step(Block& block, const Tensor& grad, const Hyper& hyper) {
   block.g.shape = block.x.shape;
   uint64_t t = block.t;
   uint32_t upd = block.updated ? 1u : 0u;
+  if (h.c.kind == RW_LAMB) {  // step_lamb pushes its trust ratio (optim.cpp:294)
+    double trust = 0.0;
+    const int sl = rw_host_block_lamb_step(RW_F64, block.x.data.data(), block.g.data.data(), block.m.data.data(),
+                                           block.v.data.data(), n, &t, &upd, grad.data.data(), &h.c, &trust);
+    block.t = t;
+    block.updated = upd != 0;
+    if (sl == RW_OK || sl == RW_NUMERICAL_ERROR) block.saved_scalars.push_back(trust);  // before check_finite
+    detail::check(sl);
+    return;
+  }
   const int st = rw_host_block_step(RW_F64, block.x.data.data(), block.g.data.data(),
                                     block.m.data.data(), block.v.data.data(),
                                     h.c.kind == RW_AMSGRAD ? block.vmax.data.data() : nullptr, n, &t,
@@ -148,6 +158,17 @@ void optimizer_undo(Block& block, const Hyper& hyper) {
   const uint64_t n = block.x.data.size();
   uint64_t t = block.t;
   uint32_t upd = block.updated ? 1u : 0u;
+  if (h.c.kind == RW_LAMB) {  // undo_lamb consumes the top ratio (optim.cpp:305-319)
+    const bool have = !block.saved_scalars.empty();
+    const int sl = rw_host_block_lamb_undo(RW_F64, block.x.data.data(), detail::ptr_or_null(block.g),
+                                           detail::ptr_or_null(block.m), detail::ptr_or_null(block.v), n, &t, &upd,
+                                           &h.c, have ? 1u : 0u, have ? block.saved_scalars.back() : 0.0);
+    block.t = t;
+    block.updated = upd != 0;
+    if (sl == RW_OK || sl == RW_NUMERICAL_ERROR) block.saved_scalars.pop_back();
+    detail::check(sl);
+    return;
+  }
   const int st = rw_host_block_undo(RW_F64, block.x.data.data(), detail::ptr_or_null(block.g),
                                     detail::ptr_or_null(block.m), detail::ptr_or_null(block.v), n,
                                     &t, &upd, &h.c);

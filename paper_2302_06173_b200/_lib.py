@@ -112,6 +112,12 @@ def _load() -> C.CDLL:
         "rw_host_block_step": (C.c_int, [i32, vp, vp, vp, vp, vp, u64, P(u64), P(u32), vp,
                                          P(rw_hyper)]),
         "rw_host_block_undo": (C.c_int, [i32, vp, vp, vp, vp, u64, P(u64), P(u32), P(rw_hyper)]),
+        "rw_host_block_lamb_step": (C.c_int, [i32, vp, vp, vp, vp, u64, P(u64), P(u32), vp,
+                                              P(rw_hyper), P(dbl)]),
+        "rw_host_block_lamb_undo": (C.c_int, [i32, vp, vp, vp, vp, u64, P(u64), P(u32),
+                                              P(rw_hyper), u32, dbl]),
+        "rw_state_saved_scalars": (C.c_int, [vp, u32, P(dbl), u32, P(u32), vp]),
+        "rw_state_set_saved_scalars": (C.c_int, [vp, u32, P(dbl), u32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

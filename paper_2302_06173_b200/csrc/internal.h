@@ -70,6 +70,13 @@ int launch_ordered_sum(int dtype, const void* const* tensors, uint32_t count, ui
                        void* stream);
 int launch_clear_updated(rw_group* groups, const uint32_t* ids, uint32_t n, void* stream);
 
+// lamb_kernels.cu: LAMB step pass 1 (m, v, norms) + trust ratio for one group;
+// writes trust to *trust_out and scaled = eta * trust into *set_dev.
+int lamb_parts_for(uint64_t len);
+int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, uint64_t off, uint64_t len,
+                      const ScalarSet& ss, const Uniform& u, double* partial, double* trust_out,
+                      ScalarSet* set_dev, void* stream);
+
 // log_kernels.cu: CRC32 (wire.cpp:31-38) of a device buffer into *out_dev;
 // scratch = crc32_scratch_words(n) device uint32 words
 int launch_crc32(const void* data, uint64_t n, uint32_t* out_dev, uint32_t* scratch, void* stream);

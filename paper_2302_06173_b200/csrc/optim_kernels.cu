@@ -145,13 +145,33 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
       v = A::div(A::sub(v, A::mul(A::mul(s.omb2, gd), gd)), s.b2);
       x = xt;
     }
+  } else if constexpr (KIND == RW_LAMB) {
+    // s.eta carries scaled = eta * trust (the saved ratio) for LAMB.
+    if constexpr (!UNDO) {
+      // second pass of step_lamb, optim.cpp:282-293: m, v already advanced
+      // by lamb_pass1_kernel; x -= (eta * trust) * update
+      T mhat = A::div(m, s.c1);
+      T vhat = A::div(v, s.c2);
+      T u = A::add(A::div(mhat, A::add(A::sqrt(vhat), s.eps)), A::mul(s.wd, x));
+      x = A::sub(x, A::mul(s.eta, u));
+    } else {
+      // optim.cpp:309-318 with scaled = eta * trust, denom = 1 - scaled * wd
+      T mhat = A::div(m, s.c1);
+      T vhat = A::div(v, s.c2);
+      T r = A::div(mhat, A::add(A::sqrt(vhat), s.eps));
+      T xt = A::div(A::add(x, A::mul(s.eta, r)), s.denom);
+      T gd = g;
+      m = A::div(A::sub(m, A::mul(s.omb1, gd)), s.b1);
+      v = A::div(A::sub(v, A::mul(A::mul(s.omb2, gd), gd)), s.b2);
+      x = xt;
+    }
   }
 }
 
 template <int KIND>
 struct Uses {
   static constexpr bool m = KIND != RW_SGD;
-  static constexpr bool v = KIND == RW_ADAM || KIND == RW_ADAMW || KIND == RW_AMSGRAD;
+  static constexpr bool v = KIND == RW_ADAM || KIND == RW_ADAMW || KIND == RW_AMSGRAD || KIND == RW_LAMB;
   static constexpr bool vmax = KIND == RW_AMSGRAD;
   static constexpr int slots = vmax ? 5 : 4;
 };
@@ -531,7 +551,7 @@ template <typename T, int KIND>
 int launch_kind(const LaunchArgs& a, cudaStream_t st) {
   const bool copy = a.grad != nullptr && a.grad != a.g;
   if (a.undo) {
-    if constexpr (KIND == RW_AMSGRAD || KIND == RW_LAMB) {
+    if constexpr (KIND == RW_AMSGRAD) {
       return static_cast<int>(cudaErrorInvalidValue);
     } else {
       if (a.px) return launch_t<T, KIND, true, false, true>(a, st);
@@ -539,7 +559,8 @@ int launch_kind(const LaunchArgs& a, cudaStream_t st) {
     }
   }
   if constexpr (KIND == RW_LAMB) {
-    return static_cast<int>(cudaErrorInvalidValue);
+    // LAMB step pass 2 (x only); the gradient was cached by lamb_pass1_kernel
+    return launch_t<T, KIND, false, false>(a, st);
   } else {
     return copy ? launch_t<T, KIND, false, true>(a, st) : launch_t<T, KIND, false, false>(a, st);
   }
@@ -553,6 +574,7 @@ int launch_dtype(const LaunchArgs& a, cudaStream_t st) {
     case RW_ADAM: return launch_kind<T, RW_ADAM>(a, st);
     case RW_ADAMW: return launch_kind<T, RW_ADAMW>(a, st);
     case RW_AMSGRAD: return launch_kind<T, RW_AMSGRAD>(a, st);
+    case RW_LAMB: return launch_kind<T, RW_LAMB>(a, st);
     default: return static_cast<int>(cudaErrorInvalidValue);
   }
 }

@@ -60,10 +60,12 @@ int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad
     }
   }
   // undo_<kind> hyper guards (optim.cpp:184, :200, :222, :252-256) and the
-  // AMSGrad refusal (:368-370); LAMB is not on the B200 path yet.
-  bool blocked = rw_invertibility_check(h->kind) != RW_INVERTIBLE;
+  // AMSGrad refusal (:368-370).  LAMB undoes with its saved trust ratio
+  // (:297-320); a group whose ratio is missing fails at apply time.
+  bool blocked = rw_invertibility_check(h->kind) == RW_NOT_INVERTIBLE_KIND;
   if (h->kind == RW_SGDM && h->momentum == 0.0) blocked = true;
-  if ((h->kind == RW_ADAM || h->kind == RW_ADAMW) && (h->beta1 == 0.0 || h->beta2 == 0.0)) blocked = true;
+  if ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB) && (h->beta1 == 0.0 || h->beta2 == 0.0))
+    blocked = true;
   s.undo_blocked = blocked ? 1 : 0;
   s.t_min = lo;
   *out = s;

@@ -85,6 +85,7 @@ struct Slot {
   bool used = false;
 };
 constexpr int kSlots = 8;
+constexpr uint32_t kTrustDepth = RW_LAMB_TRUST_DEPTH;
 
 }  // namespace
 
@@ -105,6 +106,13 @@ struct rw_state {
   rw_group* d_groups = nullptr;
   Slot slots[kSlots];
   int next_slot = 0;
+  // LAMB saved scalars (ParamBlock::saved_scalars, optim.cpp:294): a per-group
+  // ring of the last kTrustDepth trust ratios, written by lamb_trust_kernel;
+  // head/count are host-side so the stack top is known without a sync.
+  double* d_trust = nullptr;       // [G * kTrustDepth]
+  double* d_partial = nullptr;     // pass-1 scratch, 2 doubles per CTA
+  std::vector<uint64_t> trust_head;
+  std::vector<uint32_t> trust_count;
 };
 
 namespace {
@@ -170,14 +178,16 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
   Slot& sl = s->slots[s->next_slot];
   s->next_slot = (s->next_slot + 1) % kSlots;
 
-  // distinct scalar sets by tt
+  // distinct scalar sets by tt; LAMB: one set per item (eta = eta * trust)
+  const bool lamb = h->kind == RW_LAMB;
   std::map<uint64_t, uint32_t> set_of;
   for (uint32_t i = 0; i < n; ++i) {
     const rw_group& gr = s->mirror[ids[i]];
     const uint64_t tt = undo ? gr.t : gr.t + 1;
     set_of.emplace(tt, 0);
   }
-  int st = ensure_slot(s, sl, n, static_cast<uint32_t>(set_of.size()));
+  const uint32_t n_sets = lamb ? n : static_cast<uint32_t>(set_of.size());
+  int st = ensure_slot(s, sl, n, n_sets);
   if (st) return st;
   {
     uint32_t k = 0;
@@ -187,7 +197,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     if (copy_only && copy_only[i]) continue;  // pass-through groups use no scalars
     const rw_group& gr = s->mirror[ids[i]];
     const uint64_t tt = undo ? gr.t : gr.t + 1;
-    sl.h_sets[set_of[tt]] = scalars_at(h, tt, etas[i]);
+    sl.h_sets[lamb ? i : set_of[tt]] = scalars_at(h, tt, etas[i]);
   }
   const uint32_t ce = rwb::chunk_elems_for(s->dtype);
   uint64_t chunk = 0;
@@ -201,7 +211,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     w.new_t = undo ? gr.t - 1 : gr.t + 1;
     w.nchunks = static_cast<uint32_t>((gr.len + ce - 1) / ce);
     w.chunk_begin = static_cast<uint32_t>(chunk);
-    w.sidx = set_of[undo ? gr.t : gr.t + 1];
+    w.sidx = lamb ? i : set_of[undo ? gr.t : gr.t + 1];
     w.flags = (copy_only && copy_only[i]) ? rwb::kWorkCopyOnly : 0u;
     w.pad = 0;
     chunk += w.nchunks;
@@ -211,8 +221,21 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
   if (n_items > 0) {
     RW_CUDA(cudaMemcpyAsync(sl.d_work, sl.h_work, sizeof(rwb::WorkItem) * n_items,
                             cudaMemcpyHostToDevice, cs));
-    RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * set_of.size(),
+    RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * n_sets,
                             cudaMemcpyHostToDevice, cs));
+    if (lamb && !undo) {
+      // step_lamb first pass per group: m, v, both norms, trust -> d_sets[i]
+      const rwb::Uniform u = uniform_of(h);
+      for (uint32_t i = 0; i < n; ++i) {
+        const rw_group& gr = s->mirror[ids[i]];
+        const uint64_t slot = s->trust_head[ids[i]] % kTrustDepth;
+        int e = rwb::launch_lamb_pass1(s->dtype, s->x, s->g, grad == s->g ? nullptr : grad, s->m, s->v, gr.offset,
+                                       gr.len, sl.h_sets[i], u, s->d_partial,
+                                       s->d_trust + uint64_t(ids[i]) * kTrustDepth + slot, sl.d_sets + i, stream);
+        if (e) return cuda_fail(static_cast<cudaError_t>(e), "lamb pass 1");
+      }
+      grad = nullptr;  // pass 1 cached it in g
+    }
     rwb::LaunchArgs a;
     a.dtype = s->dtype;
     a.kind = h->kind;
@@ -246,6 +269,16 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     rw_group& gr = s->mirror[ids[i]];
     gr.t = undo ? gr.t - 1 : gr.t + 1;
     gr.updated = undo ? 0u : 1u;
+    if (lamb) {  // push / pop the saved trust ratio (optim.cpp:294 / :319)
+      const uint32_t g = ids[i];
+      if (undo) {
+        s->trust_head[g] -= 1;
+        s->trust_count[g] -= 1;
+      } else {
+        s->trust_head[g] += 1;
+        s->trust_count[g] = std::min(s->trust_count[g] + 1, kTrustDepth);
+      }
+    }
   }
   RW_CUDA(cudaEventRecord(sl.ev, cs));
   sl.used = true;
@@ -253,6 +286,33 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
 }
 
 size_t elem_size(int dtype) { return dtype == RW_F64 ? 8 : 4; }
+
+// undo_lamb guards (optim.cpp:297-308) for the groups ids[0..n): the saved
+// trust ratio must exist; etas[i] (lr_at(t)) becomes scaled = eta * trust and
+// denom = 1 - scaled * wd must not vanish.  One D2H read of the trust table.
+int lamb_undo_scalars(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, std::vector<double>& etas,
+                      void* stream) {
+  if (h->beta1 == 0.0 || h->beta2 == 0.0)
+    return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for lamb");
+  for (uint32_t i = 0; i < n; ++i)
+    if (s->trust_count[ids[i]] == 0)
+      return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: no saved trust ratio for lamb undo (group %u)", ids[i]);
+  if (n == 0) return RW_OK;
+  std::vector<double> tr(s->mirror.size() * kTrustDepth);
+  RW_CUDA(cudaSetDevice(s->device));
+  auto cs = static_cast<cudaStream_t>(stream);
+  RW_CUDA(cudaMemcpyAsync(tr.data(), s->d_trust, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost, cs));
+  RW_CUDA(cudaStreamSynchronize(cs));
+  for (uint32_t i = 0; i < n; ++i) {
+    const uint32_t g = ids[i];
+    const double trust = tr[uint64_t(g) * kTrustDepth + (s->trust_head[g] - 1) % kTrustDepth];
+    const double scaled = etas[i] * trust;
+    if (1.0 - scaled * h->weight_decay == 0.0)
+      return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: trust*lr*weight_decay == 1 for lamb (group %u)", g);
+    etas[i] = scaled;
+  }
+  return RW_OK;
+}
 
 }  // namespace
 
@@ -338,8 +398,13 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
   s->total = total;
   s->mirror.assign(groups, groups + n_groups);
   for (auto& gr : s->mirror) gr.flags = 0;
+  s->trust_head.assign(n_groups, 0);
+  s->trust_count.assign(n_groups, 0);
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_groups, sizeof(rw_group) * n_groups);
+  if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_trust, sizeof(double) * n_groups * kTrustDepth);
+  if (e == cudaSuccess && n_groups) e = cudaMemset(s->d_trust, 0, sizeof(double) * n_groups * kTrustDepth);
+  if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_partial, sizeof(double) * 2 * 4096);
   if (e == cudaSuccess && n_groups)
     e = cudaMemcpy(s->d_groups, s->mirror.data(), sizeof(rw_group) * n_groups, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -365,6 +430,8 @@ void rw_state_destroy(rw_state* s) {
     cudaFree(sl.d_done);
   }
   cudaFree(s->d_groups);
+  cudaFree(s->d_trust);
+  cudaFree(s->d_partial);
   delete s;
 }
 
@@ -380,6 +447,38 @@ void* rw_state_ptr(rw_state* s, int which) {
     case 4: return s->vmax;
   }
   return nullptr;
+}
+
+int rw_state_saved_scalars(rw_state* s, uint32_t group, double* out, uint32_t cap, uint32_t* count,
+                           void* stream) {
+  if (!s || !count || (cap && !out)) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (group >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", group);
+  const uint32_t c = s->trust_count[group];
+  *count = c;
+  if (c == 0 || cap == 0) return RW_OK;
+  double ring[kTrustDepth];
+  RW_CUDA(cudaSetDevice(s->device));
+  auto cs = static_cast<cudaStream_t>(stream);
+  RW_CUDA(cudaMemcpyAsync(ring, s->d_trust + uint64_t(group) * kTrustDepth, sizeof(ring), cudaMemcpyDeviceToHost, cs));
+  RW_CUDA(cudaStreamSynchronize(cs));
+  const uint64_t head = s->trust_head[group];
+  for (uint32_t k = 0; k < c && k < cap; ++k) out[k] = ring[(head - c + k) % kTrustDepth];
+  return RW_OK;
+}
+
+int rw_state_set_saved_scalars(rw_state* s, uint32_t group, const double* in, uint32_t count, void* stream) {
+  if (!s || (count && !in)) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (group >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", group);
+  if (count > kTrustDepth) return fail(RW_TOO_LARGE, "TooLarge: at most %u saved scalars per group", kTrustDepth);
+  double ring[kTrustDepth] = {};
+  for (uint32_t k = 0; k < count; ++k) ring[k] = in[k];
+  RW_CUDA(cudaSetDevice(s->device));
+  auto cs = static_cast<cudaStream_t>(stream);
+  RW_CUDA(cudaMemcpyAsync(s->d_trust + uint64_t(group) * kTrustDepth, ring, sizeof(ring), cudaMemcpyHostToDevice, cs));
+  RW_CUDA(cudaStreamSynchronize(cs));
+  s->trust_head[group] = count;
+  s->trust_count[group] = count;
+  return RW_OK;
 }
 
 int rw_state_read_groups(rw_state* s, rw_group* out, void* stream) {
@@ -476,8 +575,6 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint3
       return st;
     }
   }
-  if (h->kind == RW_LAMB)
-    return fail(RW_INVALID_ARGUMENT, "lamb step is not on the B200 path yet (SURVEY §8f rank 2)");
   if (h->kind == RW_AMSGRAD && !s->vmax) return fail(RW_INVALID_ARGUMENT, "amsgrad needs a vmax buffer");
   if ((h->kind != RW_SGD && !s->m) ||
       ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_AMSGRAD) && !s->v))
@@ -519,15 +616,22 @@ int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint3
         if (1.0 - eta * h->weight_decay == 0.0)
           return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1 for adamw");
         break;
-      case RW_LAMB:
+      case RW_LAMB:  // optim.cpp:297-303; the trust read + denom check follow the loop
         if (h->beta1 == 0.0 || h->beta2 == 0.0)
           return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for lamb");
-        return fail(RW_INVALID_ARGUMENT, "lamb undo is not on the B200 path yet (SURVEY §8f rank 2)");
+        if (s->trust_count[ids[i]] == 0)
+          return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: no saved trust ratio for lamb undo (group %u)", ids[i]);
+        break;
       default: return fail(RW_INVALID_ARGUMENT, "unknown optimizer kind %d", h->kind);
     }
   }
-  if ((h->kind != RW_SGD && !s->m) || ((h->kind == RW_ADAM || h->kind == RW_ADAMW) && !s->v))
+  if ((h->kind != RW_SGD && !s->m) ||
+      ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB) && !s->v))
     return fail(RW_INVALID_ARGUMENT, "%s needs m/v buffers", kind_name(h->kind));
+  if (h->kind == RW_LAMB) {
+    int st = lamb_undo_scalars(s, h, ids, n, etas, stream);
+    if (st) return st;
+  }
   return launch_groups(s, h, ids, n, true, nullptr, etas, stream);
 }
 
@@ -630,7 +734,8 @@ int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* 
   const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_AMSGRAD;
   if ((um && !m) || (uv && !v) || (h->kind == RW_AMSGRAD && !vmax))
     return fail(RW_INVALID_ARGUMENT, "%s needs its m/v/vmax buffers", kind_name(h->kind));
-  if (h->kind == RW_LAMB) return fail(RW_INVALID_ARGUMENT, "lamb is not on the B200 path yet (SURVEY §8f rank 2)");
+  if (h->kind == RW_LAMB)
+    return fail(RW_INVALID_ARGUMENT, "lamb needs the saved-scalar stack: use rw_host_block_lamb_step");
   st = stage_prepare(dtype, n);
   if (st) return st;
   HostStage& S = g_stage;
@@ -663,6 +768,8 @@ int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64
   // call never touches the device.
   if (!*updated) return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: block has no pending update");
   if (h->kind == RW_AMSGRAD) return fail(RW_NOT_INVERTIBLE, "NotInvertible: amsgrad element-wise max has no inverse");
+  if (h->kind == RW_LAMB)
+    return fail(RW_INVALID_ARGUMENT, "lamb needs the saved-scalar stack: use rw_host_block_lamb_undo");
   const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW;
   if ((um && !m) || (uv && !v)) return fail(RW_INVALID_ARGUMENT, "%s needs its m/v buffers", kind_name(h->kind));
   int st = stage_prepare(dtype, n);
@@ -685,6 +792,78 @@ int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64
   *t -= 1;  // optim.cpp:380-381
   *updated = 0;
   return rw_state_check(S.st, S.stream);  // :382-384, after mutation
+}
+
+int rw_host_block_lamb_step(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
+                            uint32_t* updated, const void* grad, const rw_hyper* h, double* trust_out) {
+  if (!x || !g || !m || !v || !t || !updated || !h || !grad || !trust_out)
+    return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (h->kind != RW_LAMB) return fail(RW_INVALID_ARGUMENT, "rw_host_block_lamb_step needs kind RW_LAMB");
+  if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "bad dtype");
+  if (n == 0) return fail(RW_INVALID_SHAPE, "InvalidShape: zero extent");
+  const size_t bytes = n * elem_size(dtype);
+  double eta = 0;
+  int st = block_guards_step(h, *t, *updated, &eta);
+  if (st) {
+    if (st == RW_INVALID_CONFIG) std::memcpy(g, grad, bytes);
+    return st;
+  }
+  st = stage_prepare(dtype, n);
+  if (st) return st;
+  HostStage& S = g_stage;
+  void* hs[4] = {x, const_cast<void*>(grad), m, v};
+  for (int i = 0; i < 4; ++i) RW_CUDA(cudaMemcpyAsync(S.d[i], hs[i], bytes, cudaMemcpyHostToDevice, S.stream));
+  rw_group gr{0, n, *t, 0, 0};
+  st = rw_state_write_groups(S.st, &gr, S.stream);
+  if (st) return st;
+  st = rw_state_set_saved_scalars(S.st, 0, nullptr, 0, S.stream);
+  if (st) return st;
+  const uint32_t id = 0;
+  st = rw_optimizer_step(S.st, h, &id, 1, nullptr, UINT32_MAX, S.stream);
+  if (st) return st;
+  void* outs[4] = {x, g, m, v};
+  for (int i = 0; i < 4; ++i) RW_CUDA(cudaMemcpyAsync(outs[i], S.d[i], bytes, cudaMemcpyDeviceToHost, S.stream));
+  uint32_t cnt = 0;
+  st = rw_state_saved_scalars(S.st, 0, trust_out, 1, &cnt, S.stream);
+  if (st) return st;
+  *t += 1;
+  *updated = 1;
+  return rw_state_check(S.st, S.stream);
+}
+
+int rw_host_block_lamb_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
+                            uint32_t* updated, const rw_hyper* h, uint32_t have_saved, double trust) {
+  if (!x || !g || !m || !v || !t || !updated || !h) return fail(RW_INVALID_ARGUMENT, "null argument");
+  if (h->kind != RW_LAMB) return fail(RW_INVALID_ARGUMENT, "rw_host_block_lamb_undo needs kind RW_LAMB");
+  if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "bad dtype");
+  if (n == 0) return fail(RW_INVALID_SHAPE, "InvalidShape: zero extent");
+  if (!*updated) return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: block has no pending update");
+  double eta = 0;
+  int st = lr_at(h, *t, &eta);
+  if (st) return st;
+  if (h->beta1 == 0.0 || h->beta2 == 0.0)
+    return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for lamb");
+  if (!have_saved) return fail(RW_NOTHING_TO_UNDO, "NothingToUndo: no saved trust ratio for lamb undo");
+  st = stage_prepare(dtype, n);
+  if (st) return st;
+  HostStage& S = g_stage;
+  const size_t bytes = n * elem_size(dtype);
+  rw_group gr{0, n, *t, 1, 0};
+  st = rw_state_write_groups(S.st, &gr, S.stream);
+  if (st) return st;
+  st = rw_state_set_saved_scalars(S.st, 0, &trust, 1, S.stream);
+  if (st) return st;
+  void* hs[4] = {x, g, m, v};
+  for (int i = 0; i < 4; ++i) RW_CUDA(cudaMemcpyAsync(S.d[i], hs[i], bytes, cudaMemcpyHostToDevice, S.stream));
+  const uint32_t id = 0;
+  st = rw_optimizer_undo(S.st, h, &id, 1, S.stream);
+  if (st) return st;
+  const bool out[4] = {true, false, true, true};
+  for (int i = 0; i < 4; ++i)
+    if (out[i]) RW_CUDA(cudaMemcpyAsync(hs[i], S.d[i], bytes, cudaMemcpyDeviceToHost, S.stream));
+  *t -= 1;
+  *updated = 0;
+  return rw_state_check(S.st, S.stream);
 }
 
 }  // extern "C"
@@ -743,7 +922,7 @@ int rw_ipc_close(void* base) {
 int rw_undo_and_push(rw_state* s, const rw_hyper* h, const uint32_t* undo_ids, uint32_t n_undo, void* peer_x,
                      void* peer_g, void* peer_m, void* peer_v, void* stream) {
   if (!s || !h || !peer_x || (n_undo && !undo_ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
-  const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW;
+  const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB;
   if ((um && !peer_m) || (uv && !peer_v)) return fail(RW_INVALID_ARGUMENT, "peer m/v buffers required");
   const uint32_t G = static_cast<uint32_t>(s->mirror.size());
   std::vector<uint8_t> is_undo(G, 0);
@@ -766,7 +945,10 @@ int rw_undo_and_push(rw_state* s, const rw_hyper* h, const uint32_t* undo_ids, u
       return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0");
     if ((h->kind == RW_SGD || h->kind == RW_ADAMW) && 1.0 - etas_u[i] * h->weight_decay == 0.0)
       return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1");
-    if (h->kind == RW_LAMB) return fail(RW_INVALID_ARGUMENT, "lamb is not on the B200 path yet");
+  }
+  if (h->kind == RW_LAMB) {
+    int st = lamb_undo_scalars(s, h, undo_ids, n_undo, etas_u, stream);
+    if (st) return st;
   }
   // every group, in layout order: undo groups flagged, the rest copy-only
   std::vector<uint32_t> ids(G);

@@ -27,6 +27,9 @@ _KIND_NAMES = {"sgd": SGD, "sgdm": SGDM, "sgd_momentum": SGDM, "adam": ADAM, "ad
                "lamb": LAMB, "amsgrad": AMSGRAD}
 
 
+TRUST_DEPTH = 8  # RW_LAMB_TRUST_DEPTH (include/rewind_b200.h)
+
+
 def optimizer_from_name(name: str) -> int | None:
     """optimizer_from_name, optim.cpp:103-111."""
     return _KIND_NAMES.get(name)
@@ -214,6 +217,18 @@ class DeviceState:
         for r, (t, u) in zip(g, markers):
             r.t, r.updated, r.flags = int(t), int(u), 0
         check(LIB.rw_state_write_groups(self._h, g, C.c_void_p(_stream_handle(stream))))
+
+    def saved_scalars(self, i: int, stream=None) -> list[float]:
+        """LAMB trust-ratio stack of group i, bottom -> top (optim.cpp:294)."""
+        buf = (C.c_double * TRUST_DEPTH)()
+        cnt = C.c_uint32()
+        check(LIB.rw_state_saved_scalars(self._h, i, buf, TRUST_DEPTH, C.byref(cnt),
+                                         C.c_void_p(_stream_handle(stream))))
+        return list(buf[:cnt.value])
+
+    def set_saved_scalars(self, i: int, vals: Sequence[float], stream=None) -> None:
+        arr = (C.c_double * max(len(vals), 1))(*vals)
+        check(LIB.rw_state_set_saved_scalars(self._h, i, arr, len(vals), C.c_void_p(_stream_handle(stream))))
 
     @property
     def handle(self) -> C.c_void_p:

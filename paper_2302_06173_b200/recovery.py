@@ -116,17 +116,18 @@ def apply_resolution(state, hyper, plan: ResolvePlan, grad: torch.Tensor | None 
     if plan.strategy == STRATEGY_NAMES[STRATEGY_GLOBAL_ROLLBACK]:
         raise RwError(101, "plan requires a global checkpoint rollback (SPEC:488)")
     if plan.strategy == STRATEGY_NAMES[STRATEGY_UNDO] and plan.undo_ids:
+        undo = set(plan.undo_ids)
         mk = state.markers(stream)
-        if any(mk[i][1] == 0 for i in plan.undo_ids):
-            state.write_markers([(t, 1 if i in set(plan.undo_ids) else u)
-                                 for i, (t, u) in enumerate(mk)], stream)
+        if any(mk[i][1] == 0 for i in undo):
+            state.write_markers([(t, 1 if i in undo else u) for i, (t, u) in enumerate(mk)], stream)
         # undo in reverse update order (first layer's update was the last)
-        order = [i for i in reversed(state.update_order()) if i in set(plan.undo_ids)]
+        order = [i for i in reversed(state.update_order()) if i in undo]
         state.undo(hyper, order, stream=stream)
     elif plan.strategy == STRATEGY_NAMES[STRATEGY_REDO] and plan.redo_ids:
         if grad is None:
             raise RwError(101, "redo needs the synchronised gradient buffer")
-        order = [i for i in state.update_order() if i in set(plan.redo_ids)]
+        redo = set(plan.redo_ids)
+        order = [i for i in state.update_order() if i in redo]
         state.step(hyper, order, grad=grad, stream=stream)
 
 
@@ -201,6 +202,7 @@ def recover_replication_fused(state, hyper, plan: ResolvePlan, src: int, include
         LAST_FUSED_INFO.clear()
         LAST_FUSED_INFO.update(map_ms=(t1 - t0) * 1e3, kernel_ms=e0.elapsed_time(e1))
     dist.barrier(group=group)
+    _broadcast_saved_scalars(state, src, group)
     mk = state.markers()
     backend = dist.get_backend(group)
     dev = state.device if backend == "nccl" else torch.device("cpu")
@@ -209,6 +211,31 @@ def recover_replication_fused(state, hyper, plan: ResolvePlan, src: int, include
     flat = t.cpu().tolist()
     state.write_markers([(flat[2 * i], flat[2 * i + 1]) for i in range(len(mk))])
     return nbytes
+
+
+def _broadcast_saved_scalars(state, src: int, group=None) -> None:
+    """LAMB: the replacement needs the survivor's trust-ratio stacks
+    (ParamBlock::saved_scalars) for a later undo — one small broadcast."""
+    from ._lib import LAMB
+    from .optim import TRUST_DEPTH
+    if getattr(state, "kind", None) != LAMB:
+        return
+    G = state.num_groups
+    backend = dist.get_backend(group)
+    dev = state.device if backend == "nccl" else torch.device("cpu")
+    buf = torch.zeros(G, 1 + TRUST_DEPTH, dtype=torch.float64)
+    if dist.get_rank(group) == src:
+        for i in range(G):
+            vals = state.saved_scalars(i)
+            buf[i, 0] = len(vals)
+            buf[i, 1:1 + len(vals)] = torch.tensor(vals, dtype=torch.float64)
+    t = buf.to(dev)
+    dist.broadcast(t, src=src, group=group)
+    if dist.get_rank(group) != src:
+        rows = t.cpu()
+        for i in range(G):
+            c = int(rows[i, 0])
+            state.set_saved_scalars(i, rows[i, 1:1 + c].tolist())
 
 
 def recover_replication(state, src: int, include_grad: bool = False, group=None) -> int:
@@ -222,6 +249,7 @@ def recover_replication(state, src: int, include_grad: bool = False, group=None)
     bufs += [b for b in (state.m, state.v) if b is not None]
     for b in bufs:
         dist.broadcast(b, src=src, group=group)
+    _broadcast_saved_scalars(state, src, group)
     mk = state.markers()
     backend = dist.get_backend(group)
     dev = state.device if backend == "nccl" else torch.device("cpu")

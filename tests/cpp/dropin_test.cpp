@@ -90,7 +90,22 @@ int cpu_checks() {
   EXPECT(err_of([&] { R::optimizer_step(a, g, neg); }) == err_of([&] { B::optimizer_step(b, g, neg); }),
          "InvalidConfig");
   EXPECT(same_bits(a.g, b.g), "grad cached before lr_at raises (optim.cpp:349-350)");
+  // LAMB undo with an empty saved-scalar stack (optim.cpp:305-307)
+  R::OptimizerHyper lamb = hyper(R::OptimizerKind::Lamb);
+  a.updated = b.updated = true;
+  a.t = b.t = 2;
+  EXPECT(err_of([&] { R::optimizer_undo(a, lamb); }) == err_of([&] { B::optimizer_undo(b, lamb); }),
+         "lamb NothingToUndo without a saved ratio");
   return 0;
+}
+
+static bool close_rel(const R::Tensor& a, const R::Tensor& b, double tol) {
+  if (a.data.size() != b.data.size()) return false;
+  double mx = 0;
+  for (double v : a.data) mx = std::max(mx, std::fabs(v));
+  for (std::size_t i = 0; i < a.data.size(); ++i)
+    if (std::fabs(a.data[i] - b.data[i]) > tol * mx) return false;
+  return true;
 }
 
 int gpu_checks() {
@@ -130,6 +145,34 @@ int gpu_checks() {
     EXPECT(same_bits(a.x, b.x) && same_bits(a.vmax, b.vmax), "amsgrad step");
     EXPECT(err_of([&] { R::optimizer_undo(a, h); }) == err_of([&] { B::optimizer_undo(b, h); }),
            "amsgrad undo");
+  }
+  // LAMB: m, v, g bit-exact; the trust ratio (fp64 norms, fixed tree order on
+  // the device vs a sequential sum) within 2 n 2^-53 relative, x accordingly
+  for (int trial = 0; trial < 4; ++trial) {
+    const std::size_t n = 1 + rng() % 20000;
+    R::ParamBlock a = R::ParamBlock::make({n}, rng());
+    a.m = R::seeded_fill({n}, rng());
+    a.v = R::seeded_fill({n}, rng());
+    for (double& x : a.v.data) x = std::fabs(x) * 1e-3;
+    a.t = rng() % 40;
+    R::ParamBlock b = a;
+    R::Tensor g = R::seeded_fill({n}, rng());
+    R::OptimizerHyper h = hyper(R::OptimizerKind::Lamb);
+    const double tol = 4.0 * double(n) * 0x1p-53;
+    R::optimizer_step(a, g, h);
+    B::optimizer_step(b, g, h);
+    EXPECT(same_bits(a.m, b.m) && same_bits(a.v, b.v) && same_bits(a.g, b.g), "lamb step m/v/g bit-exact");
+    EXPECT(b.saved_scalars.size() == 1 && a.saved_scalars.size() == 1 &&
+               std::fabs(a.saved_scalars[0] - b.saved_scalars[0]) <= tol * a.saved_scalars[0],
+           "lamb trust ratio");
+    EXPECT(close_rel(a.x, b.x, tol), "lamb step x");
+    EXPECT(a.t == b.t && a.updated == b.updated, "lamb step marker");
+    R::optimizer_undo(a, h);
+    B::optimizer_undo(b, h);
+    EXPECT(same_bits(a.m, b.m) && same_bits(a.v, b.v), "lamb undo m/v bit-exact");
+    EXPECT(close_rel(a.x, b.x, tol), "lamb undo x");
+    EXPECT(a.saved_scalars.empty() && b.saved_scalars.empty(), "lamb undo pops the ratio");
+    EXPECT(a.t == b.t && a.updated == b.updated, "lamb undo marker");
   }
   // NumericalError after mutation
   {
