@@ -243,13 +243,18 @@ def measure_undo(sizes, kind_name: str, steps: int, warmup: int, dtype=None, t0:
     """Device-resident undo timing: (per-undo ms list, bytes per undo, state)."""
     import torch
 
-    from paper_2302_06173_b200 import ADAM, SGDM, DeviceState, OptimizerHyper
+    from paper_2302_06173_b200 import ADAM, ADAMW, LAMB, SGD, SGDM, DeviceState, OptimizerHyper
     dtype = dtype or torch.float32
-    kind = ADAM if kind_name == "adam" else SGDM
+    kind = {"adam": ADAM, "adamw": ADAMW, "lamb": LAMB, "sgd": SGD, "sgdm": SGDM}[kind_name]
     st = DeviceState(sizes, dtype=dtype, kind=kind)
-    if kind == ADAM:
+    if kind in (ADAM, ADAMW, LAMB):
         _fill_adam_state(st)
-        h = OptimizerHyper(kind=ADAM, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+        h = OptimizerHyper(kind=kind, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    elif kind == SGD:
+        from paper_2302_06173_b200 import seeded_fill_
+        seeded_fill_(st.x, 1)
+        seeded_fill_(st.g, 2)
+        h = OptimizerHyper(kind=SGD, lr=0.1, weight_decay=1e-4)
     else:
         from paper_2302_06173_b200 import seeded_fill_
         seeded_fill_(st.x, 1)
@@ -259,7 +264,7 @@ def measure_undo(sizes, kind_name: str, steps: int, warmup: int, dtype=None, t0:
     st.write_markers([(t0, 0)] * st.num_groups)
     stream = torch.cuda.current_stream()
     es = 8 if dtype == torch.float64 else 4
-    per_elem = (7 if kind == ADAM else 5) * es
+    per_elem = {ADAM: 7, ADAMW: 7, LAMB: 7, SGDM: 5, SGD: 3}[kind] * es
     nbytes = sum(sizes) * per_elem
     for _ in range(warmup):
         st.step(h)
@@ -268,13 +273,18 @@ def measure_undo(sizes, kind_name: str, steps: int, warmup: int, dtype=None, t0:
     times = []
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(steps)]
+    sevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(steps)]
     for i in range(steps):
-        st.step(h)                       # re-arm (untimed)
+        sevs[i][0].record(stream)
+        st.step(h)                       # re-arm (timed separately)
+        sevs[i][1].record(stream)
         evs[i][0].record(stream)
         st.undo(h)                       # timed
         evs[i][1].record(stream)
     torch.cuda.synchronize()
     times = [a.elapsed_time(b) for a, b in evs]
+    measure_undo.last_step_ms = [a.elapsed_time(b) for a, b in sevs]
     st.check_finite()
     return times, nbytes, st, h
 
@@ -327,7 +337,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     import torch.distributed as dist
 
     from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper
-    from paper_2302_06173_b200.recovery import (apply_resolution, recover_replication,
+    from paper_2302_06173_b200.recovery import (apply_resolution, recover, recover_replication,
                                                 recover_replication_fused, resolve)
     from paper_2302_06173_b200.workloads import gpt2_xl_sizes
     sizes = gpt2_xl_sizes()
@@ -336,7 +346,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     if rank == 0:
         _fill_adam_state(st)
     out = {}
-    modes = ["nccl", "fused"] if world > 1 else ["local"]
+    modes = ["nccl", "fused", "auto"] if world > 1 else ["local"]
     for mode in modes:
         res = []
         kinfo = []
@@ -350,7 +360,10 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
             t_wall = time.perf_counter()
             plan = resolve(st.markers() if rank == 0 else [], h, lens=sizes if rank == 0 else None,
                            device=device)
-            if mode == "fused":
+            if mode == "auto":
+                used, nbytes = recover(st, h, plan, src=0)
+                kinfo.append({"used": used})
+            elif mode == "fused":
                 nbytes = recover_replication_fused(st, h, plan, src=0)
                 if rank == 0:
                     from paper_2302_06173_b200 import recovery as _rec
@@ -372,7 +385,9 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
                          bytes_per_replacement=nbytes,
                          transfer_algbw_gbs=round(nbytes / (ms * 1e-3) / 1e9, 1) if nbytes else None,
                          frac_of_nvlink_roofline=round(nbytes / 770e9 / (ms * 1e-3), 3) if nbytes else None)
-        if kinfo:
+        if kinfo and "used" in kinfo[0]:
+            out[mode]["transfer"] = kinfo[0]["used"]
+        elif kinfo:
             km = statistics.median(k["kernel_ms"] for k in kinfo[1:] or kinfo)
             out[mode]["push_kernel_ms"] = round(km, 3)
             out[mode]["push_kernel_gbs"] = round(nbytes / (km * 1e-3) / 1e9, 1)
@@ -500,6 +515,16 @@ def run_b200(args) -> None:
             msg = statistics.median(tsg)
             extras["sgdm10m_undo_all"] = dict(ms=round(msg, 4),
                                               gbs=round(nbsg / (msg * 1e-3) / 1e9, 1))
+            # the other kinds of Table 1 on the same 336M BERT-large layout
+            by_kind = {}
+            for kn in ("sgd", "adamw", "lamb"):
+                tk, nbk, sk, _ = measure_undo(sizes, kn, 5, 2)
+                del sk
+                torch.cuda.empty_cache()
+                mk_ = statistics.median(tk)
+                by_kind[kn] = dict(undo_ms=round(mk_, 4), undo_gbs=round(nbk / (mk_ * 1e-3) / 1e9, 1),
+                                   step_ms=round(statistics.median(measure_undo.last_step_ms), 4))
+            extras["undo_by_kind_340m"] = by_kind
         if not args.no_extras:
             try:
                 extras["recovery"] = recovery_e2e(world, rank, device)
@@ -550,6 +575,11 @@ def run_b200(args) -> None:
         "cpu_baseline": cpu,
         "extras": extras,
     }
+    rec = extras.get("recovery", {})
+    pick = rec.get("auto") or rec.get("local")
+    if pick:
+        line["recovery_ms"] = {"value": pick["recovery_ms"], "transfer": pick.get("transfer", "local undo"),
+                               "workload": "config 3 (GPT-2 XL Adam, crash after 290/580 groups)"}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

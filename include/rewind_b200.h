@@ -328,6 +328,38 @@ int rw_log_open(rw_log_reader** out, const char* path, uint32_t* machine);
  * caller on the device (rw_crc32_device) against rec->crc32. */
 int rw_log_next(rw_log_reader* r, rw_log_record* rec, void* payload, uint64_t cap, int32_t* eof);
 void rw_log_close(rw_log_reader* r);
+/* Header-only walk (payload skipped, CRC not checked): used by rw_log_gc. */
+int rw_log_skip(rw_log_reader* r, rw_log_record* rec, int32_t* eof);
+
+/* ---- global checkpoint store (no reference source) ----
+ * write: every blob of this worker (device buffers via a pinned, pipelined
+ * D2H; host buffers directly), each fsync'd, CRC32 (wire.cpp polynomial; on
+ * the GPU for device blobs) recorded in the worker manifest, which is then
+ * committed atomically.  crash_after_blobs: test hook, UINT32_MAX = none.
+ * commit: once all n_workers manifests exist, atomically publish
+ * MANIFEST_<iteration> — the checkpoint is visible iff that file exists.
+ * latest: highest committed iteration (NoCheckpoint if none).
+ * load: NoCheckpoint if the iteration is not committed; ShapeMismatch if a
+ * blob's size differs; StorageError on a missing/truncated blob or a CRC
+ * mismatch (recomputed on the GPU after the H2D). */
+typedef struct rw_blob {
+  const char* name;  /* [A-Za-z0-9._-]+ */
+  void* data;
+  uint64_t bytes;
+  uint32_t on_host;  /* 1: data is host memory */
+  uint32_t pad;
+} rw_blob;
+int rw_ckpt_write(const char* dir, uint64_t iteration, uint32_t worker, const rw_blob* blobs, uint32_t n,
+                  uint32_t crash_after_blobs, void* stream);
+int rw_ckpt_commit(const char* dir, uint64_t iteration, uint32_t n_workers);
+int rw_ckpt_latest(const char* dir, uint64_t* iteration);
+int rw_ckpt_blob_bytes(const char* dir, uint64_t iteration, uint32_t worker, const char* name, uint64_t* bytes);
+int rw_ckpt_load(const char* dir, uint64_t iteration, uint32_t worker, const rw_blob* blobs, uint32_t n,
+                 void* stream);
+/* gc_logs: delete every log chunk in log_dir whose records
+ * all have iteration < ckpt_iteration; NoCheckpoint unless that checkpoint is
+ * committed in ckpt_dir.  Idempotent. */
+int rw_log_gc(const char* log_dir, const char* ckpt_dir, uint64_t ckpt_iteration, uint32_t* deleted);
 
 /* ---- selective-logging policy (planner.cpp missing) ---- */
 /* bubble_ratio(p, m), schedule.cpp:86-93 */

@@ -406,6 +406,33 @@ int rw_log_next(rw_log_reader* r, rw_log_record* rec, void* payload, uint64_t ca
   return RW_OK;
 }
 
+int rw_log_skip(rw_log_reader* r, rw_log_record* rec, int32_t* eof) {
+  if (!r || !rec || !eof) return lfail(RW_INVALID_ARGUMENT, "null argument");
+  *eof = 0;
+  uint8_t b0;
+  if (std::fread(&b0, 1, 1, r->f) != 1) {
+    *eof = 1;
+    return RW_OK;
+  }
+  std::ungetc(b0, r->f);
+  std::memset(rec, 0, sizeof(*rec));
+  uint32_t len = 0;
+  uint8_t dir = 0, dt = 0, nd = 0, pad = 0;
+  if (!rd_le(r->f, &len) || !rd_le(r->f, &rec->sender) || !rd_le(r->f, &rec->receiver) ||
+      !rd_le(r->f, &rec->iteration) || !rd_le(r->f, &rec->mb) || !rd(r->f, &dir, 1) || !rd(r->f, &dt, 1) ||
+      !rd(r->f, &nd, 1) || !rd(r->f, &pad, 1) || nd > 4)
+    return lfail(RW_CORRUPT_LOG, "CorruptLog: truncated record header");
+  rec->direction = dir;
+  rec->dtype = dt;
+  rec->ndim = nd;
+  for (uint32_t i = 0; i < nd; ++i)
+    if (!rd_le(r->f, &rec->shape[i])) return lfail(RW_CORRUPT_LOG, "CorruptLog: truncated shape");
+  if (!rd_le(r->f, &rec->payload_bytes)) return lfail(RW_CORRUPT_LOG, "CorruptLog: truncated length");
+  if (std::fseek(r->f, static_cast<long>(rec->payload_bytes), SEEK_CUR) != 0 || !rd_le(r->f, &rec->crc32))
+    return lfail(RW_CORRUPT_LOG, "CorruptLog: truncated payload");
+  return RW_OK;
+}
+
 void rw_log_close(rw_log_reader* r) {
   if (!r) return;
   if (r->f) std::fclose(r->f);

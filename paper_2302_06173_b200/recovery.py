@@ -258,3 +258,23 @@ def recover_replication(state, src: int, include_grad: bool = False, group=None)
     flat = t.cpu().tolist()
     state.write_markers([(flat[2 * i], flat[2 * i + 1]) for i in range(len(mk))])
     return sum(b.numel() * b.element_size() for b in bufs)
+
+
+def recover(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False, group=None,
+            transfer: str = "auto") -> tuple[str, int]:
+    """apply_undo + recover_replication with the transfer picked per topology:
+    one replacement -> the fused undo + NVLink push kernel (the survivor's
+    egress feeds exactly one ingress, so the push runs at link speed and hides
+    the undo); several -> undo, then NCCL's pipelined ring broadcast (a single
+    pusher would serialise its egress over the replacements).  The fused path
+    needs every rank on one node (CUDA IPC).  Returns (transfer used, bytes
+    per replacement)."""
+    world = dist.get_world_size(group)
+    if transfer == "auto":
+        same_node = world <= torch.cuda.device_count()
+        transfer = "fused" if (world == 2 and same_node) else "nccl"
+    if transfer == "fused":
+        return transfer, recover_replication_fused(state, hyper, plan, src, include_grad, group)
+    if dist.get_rank(group) == src:
+        apply_resolution(state, hyper, plan)
+    return "nccl", recover_replication(state, src, include_grad, group)
