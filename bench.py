@@ -290,38 +290,108 @@ def measure_undo(sizes, kind_name: str, steps: int, warmup: int, dtype=None, t0:
 
 
 def measure_e2e_host(st, h, steps: int):
-    """Same metric through the C-ABI with HOST buffers: each step copies the
-    state from pinned host memory, undoes it, and reads x, m, v back."""
+    """Same metric through the C-ABI with HOST buffers: each step undoes a
+    state held in pinned host memory (rw_optimizer_undo_host: per-slice H2D of
+    x, g, m, v, the undo kernel and the D2H of x, m, v pipelined on three
+    streams), timed from the first H2D to the last D2H."""
     import torch
     stream = torch.cuda.current_stream()
-    hx = st.x.cpu().pin_memory()
-    hg = st.g.cpu().pin_memory()
-    hm = st.m.cpu().pin_memory()
-    hv = st.v.cpu().pin_memory()
-    ox, om, ov = (torch.empty_like(hx).pin_memory() for _ in range(3))
+    host = {k: getattr(st, k).cpu().pin_memory() for k in ("x", "g", "m", "v")}
+    out = {k: torch.empty_like(host[k]).pin_memory() for k in ("x", "m", "v")}
     mk = st.markers()
     armed = [(t, 1) for t, _ in mk]
-    h2d = sum(b.numel() * b.element_size() for b in (hx, hg, hm, hv))
-    d2h = sum(b.numel() * b.element_size() for b in (ox, om, ov))
+    h2d = sum(b.numel() * b.element_size() for b in host.values())
+    d2h = sum(b.numel() * b.element_size() for b in out.values())
     times = []
-    for _ in range(steps):
+    for _ in range(steps + 1):
+        st.write_markers(armed)          # the host ParamBlocks arrive with updated=1
         torch.cuda.synchronize()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record(stream)
-        st.x.copy_(hx, non_blocking=True)
-        st.g.copy_(hg, non_blocking=True)
-        st.m.copy_(hm, non_blocking=True)
-        st.v.copy_(hv, non_blocking=True)
-        st.write_markers(armed)          # the host ParamBlocks arrive with updated=1
-        st.undo(h)
-        ox.copy_(st.x, non_blocking=True)
-        om.copy_(st.m, non_blocking=True)
-        ov.copy_(st.v, non_blocking=True)
+        st.undo_from_host(h, host, out)
         t1.record(stream)
         torch.cuda.synchronize()
         times.append(t0.elapsed_time(t1))
-    return times, h2d, d2h
+    return times[1:], h2d, d2h
+
+
+def pcie_probe(nbytes: int = 1 << 30) -> dict:
+    """Pinned-memory copy bandwidths on this box: the e2e roofline."""
+    import torch
+    hb = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    hb2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    db = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    db2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(fn):
+        best = 1e9
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            best = min(best, time.perf_counter() - t0)
+        return best
+    th = timed(lambda: db.copy_(hb, non_blocking=True))
+    td = timed(lambda: hb.copy_(db, non_blocking=True))
+
+    def both():
+        with torch.cuda.stream(s1):
+            db.copy_(hb, non_blocking=True)
+        with torch.cuda.stream(s2):
+            hb2.copy_(db2, non_blocking=True)
+    tb = timed(both)
+    return dict(h2d_gbs=round(nbytes / th / 1e9, 1), d2h_gbs=round(nbytes / td / 1e9, 1),
+                bidir_gbs_each=round(nbytes / tb / 1e9, 1))
+
+
+def checkpoint_bench(sizes, reps: int = 2) -> dict:
+    """Global checkpoint write + load of the config-2 Adam state (x, m, v fp32)
+    through the native store: pinned pipelined D2H/H2D, GPU CRC32, fsync'd
+    blobs, atomic manifest.  Bound: min(PCIe, storage)."""
+    import shutil
+    import tempfile
+
+    import torch
+
+    from paper_2302_06173_b200 import ADAM, DeviceState
+    from paper_2302_06173_b200.checkpoint import load_checkpoint, write_checkpoint
+    root = os.environ.get("RW_CKPT_DIR", "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp")
+    st = DeviceState(sizes, kind=ADAM)
+    _fill_adam_state(st)
+    nbytes = 3 * st.total * 4
+    free = shutil.disk_usage(root).free
+    if free < 2.5 * nbytes:
+        root = tempfile.gettempdir()
+        if shutil.disk_usage(root).free < 2.5 * nbytes:
+            return {"skipped": f"not enough space for {nbytes} B"}
+    d = tempfile.mkdtemp(prefix="rw_ckpt_", dir=root)
+    try:
+        wt, lt = [], []
+        for r in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            write_checkpoint(st, d, 100 + r)
+            wt.append(time.perf_counter() - t0)
+            dst = DeviceState(sizes, kind=ADAM)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            load_checkpoint(dst, d, 100 + r)
+            torch.cuda.synchronize()
+            lt.append(time.perf_counter() - t0)
+            ok = torch.equal(dst.x, st.x) and torch.equal(dst.v, st.v)
+            del dst
+            shutil.rmtree(os.path.join(d, f"ck_{100 + r:016d}"), ignore_errors=True)
+        w, l_ = min(wt), min(lt)
+        return dict(bytes=nbytes, dir=root, write_s=round(w, 3), write_gbs=round(nbytes / w / 1e9, 2),
+                    load_s=round(l_, 3), load_gbs=round(nbytes / l_ / 1e9, 2), bit_exact=bool(ok),
+                    path="native pinned ring (3 x 64 MiB), GPU CRC32, fsync + atomic manifest")
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+        del st
+        torch.cuda.empty_cache()
 
 
 def recovery_e2e(world: int, rank: int, device, steps: int = 3):
@@ -491,6 +561,9 @@ def run_b200(args) -> None:
         achieved = nbytes / (mean_ms * 1e-3) / 1e9
         e2e_times, h2d, d2h = measure_e2e_host(st, h, max(1, min(args.steps, 3)))
         e2e_ms = statistics.median(e2e_times)
+        pcie = pcie_probe()
+        # roofline of the pipelined path: both directions concurrently at the bidirectional rate
+        e2e_roof_ms = max(h2d, d2h) / (pcie["bidir_gbs_each"] * 1e9) * 1e3
         e2e_val = nbytes * world / (e2e_ms * 1e-3) / 1e9
         del st
         torch.cuda.empty_cache()
@@ -525,6 +598,10 @@ def run_b200(args) -> None:
                 by_kind[kn] = dict(undo_ms=round(mk_, 4), undo_gbs=round(nbk / (mk_ * 1e-3) / 1e9, 1),
                                    step_ms=round(statistics.median(measure_undo.last_step_ms), 4))
             extras["undo_by_kind_340m"] = by_kind
+            try:
+                extras["checkpoint"] = checkpoint_bench(sizes)
+            except Exception as e:  # pragma: no cover - disk space / permissions on the box
+                extras["checkpoint"] = {"error": str(e)[:200]}
         if not args.no_extras:
             try:
                 extras["recovery"] = recovery_e2e(world, rank, device)
@@ -569,7 +646,9 @@ def run_b200(args) -> None:
                      "kernel": "optim_kernel<float, ADAM, undo>"},
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms": round(e2e_ms, 3),
-                "path": "C-ABI rw_optimizer_undo with pinned host buffers (H2D x,g,m,v; D2H x,m,v)"},
+                "pcie": pcie, "roofline_ms": round(e2e_roof_ms, 2), "frac": round(e2e_roof_ms / e2e_ms, 3),
+                "path": "C-ABI rw_optimizer_undo_host, pinned host buffers; per-slice H2D x,g,m,v | undo | D2H x,m,v "
+                        "pipelined on 3 streams"},
         "gpu_launches": 2 * args.steps,
         "clocks": clocks,
         "cpu_baseline": cpu,

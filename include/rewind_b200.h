@@ -170,6 +170,21 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* group_ids,
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
                       void* stream);
 
+/* optimizer_undo for a state that lives in HOST memory in the same flat
+ * layout (e.g. a CPU-offloaded replica): x, g, m, v are read from hx.. and
+ * the undone x, m, v written to ox.. (may alias the inputs); the device
+ * buffers of `s` are the staging area and end up holding the same result.
+ * Groups are cut into slices of ~slice_elems elements (0 = 16M) in layout
+ * order, tiling the span from the first to the last selected group (other
+ * groups inside the span pass through unchanged; nothing outside it is
+ * touched); per slice H2D, undo and D2H run on three streams as a pipeline, so
+ * both PCIe directions overlap the kernel.  Host buffers must be pinned for
+ * the copies to be asynchronous.  Guards and markers exactly as
+ * rw_optimizer_undo; ordered on `stream` (complete when it completes). */
+int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
+                           const void* hx, const void* hg, const void* hm, const void* hv, void* ox, void* om,
+                           void* ov, uint64_t slice_elems, void* stream);
+
 /* ---- replica recovery fused with the undo ----
  * CUDA IPC export/import of a device buffer so a survivor can write into a
  * replacement's HBM over NVLink.  export returns the 64-byte handle of the

@@ -116,6 +116,8 @@ def _load() -> C.CDLL:
                                               P(rw_hyper), P(dbl)]),
         "rw_host_block_lamb_undo": (C.c_int, [i32, vp, vp, vp, vp, u64, P(u64), P(u32),
                                               P(rw_hyper), u32, dbl]),
+        "rw_optimizer_undo_host": (C.c_int, [vp, P(rw_hyper), P(u32), u32, vp, vp, vp, vp, vp, vp, vp, u64,
+                                             vp]),
         "rw_state_saved_scalars": (C.c_int, [vp, u32, P(dbl), u32, P(u32), vp]),
         "rw_state_set_saved_scalars": (C.c_int, [vp, u32, P(dbl), u32, vp]),
     }

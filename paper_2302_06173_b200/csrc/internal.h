@@ -70,12 +70,13 @@ int launch_ordered_sum(int dtype, const void* const* tensors, uint32_t count, ui
                        void* stream);
 int launch_clear_updated(rw_group* groups, const uint32_t* ids, uint32_t n, void* stream);
 
-// lamb_kernels.cu: LAMB step pass 1 (m, v, norms) + trust ratio for one group;
-// writes trust to *trust_out and scaled = eta * trust into *set_dev.
-int lamb_parts_for(uint64_t len);
-int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, uint64_t off, uint64_t len,
-                      const ScalarSet& ss, const Uniform& u, double* partial, double* trust_out,
-                      ScalarSet* set_dev, void* stream);
+// lamb_kernels.cu: LAMB step pass 1 (m, v and both norms) over the work list
+// + one trust CTA per item: trust -> trust_table[gid * depth + item.pad],
+// sets[item.sidx].eta *= trust (scaled), .denom = 1 - scaled * wd.
+// partial: 2 doubles per chunk.
+int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, const WorkItem* work,
+                      uint32_t n_work, uint32_t total_chunks, uint32_t chunk_elems, ScalarSet* sets,
+                      const Uniform& u, double* partial, double* trust_table, uint32_t depth, void* stream);
 
 // log_kernels.cu: CRC32 (wire.cpp:31-38) of a device buffer into *out_dev;
 // scratch = crc32_scratch_words(n) device uint32 words

@@ -1,15 +1,16 @@
 // LAMB step, first pass and trust ratio (optim.cpp:273-295).
 //
-// Pass 1 (per group): advance m, v exactly as step_lamb does, compute the
-// update r + lambda x and accumulate ||x||^2 and ||update||^2 in fp64
-// (the reference accumulates in double too).  The reduction order is fixed
-// (per-thread strided sums, a fixed block tree, a fixed final tree), so the
-// result is deterministic, but it is not the reference's left-to-right
-// sequential sum: the trust ratio agrees to ~1e-15 relative (tolerance-matched;
-// everything elementwise is bit-exact).  The trust kernel then stores the
-// ratio (the LAMB "saved scalar", optim.cpp:294) and writes scaled = eta *
-// trust into the group's ScalarSet for the elementwise pass 2 (x update),
-// which runs through the fused TMA kernel.
+// Pass 1 (all groups, one launch): advance m, v exactly as step_lamb does,
+// compute the update r + lambda x and accumulate ||x||^2 and ||update||^2 in
+// fp64 (the reference accumulates in double too).  The reduction order is
+// fixed (per-lane strided sums, a warp xor tree per chunk, per-thread strided
+// sums over a group's chunks, a block tree), so the result is deterministic,
+// but it is not the reference's left-to-right sequential sum: the trust ratio
+// agrees to ~1e-15 relative (tolerance-matched; everything elementwise is
+// bit-exact).  The trust kernel (one CTA per group) stores the ratio (the LAMB
+// "saved scalar", optim.cpp:294) and writes scaled = eta * trust into the
+// group's ScalarSet for the elementwise pass 2 (x update), which runs through
+// the fused TMA kernel.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,57 +39,90 @@ struct LA<double> {
   __device__ static double sqrt(double a) { return __dsqrt_rn(a); }
 };
 
+// vector type for 16-byte accesses
+template <typename T>
+struct V16;
+template <>
+struct V16<float> {
+  using type = float4;
+  static constexpr int n = 4;
+};
+template <>
+struct V16<double> {
+  using type = double2;
+  static constexpr int n = 2;
+};
+
+template <typename T>
+__device__ __forceinline__ void lamb_elem(const T* __restrict__ x, T* __restrict__ g, const T* __restrict__ grad,
+                                          T* __restrict__ m, T* __restrict__ v, uint64_t k, const T c1, const T c2,
+                                          const Uniform& u, double& sx, double& su) {
+  using A = LA<T>;
+  const T gd = grad ? grad[k] : g[k];
+  if (grad) g[k] = gd;  // block.g = grad (optim.cpp:349)
+  const T mk = A::add(A::mul(T(u.b1), m[k]), A::mul(T(u.one_m_b1), gd));
+  const T vk = A::add(A::mul(T(u.b2), v[k]), A::mul(A::mul(T(u.one_m_b2), gd), gd));
+  m[k] = mk;
+  v[k] = vk;
+  const T mhat = A::div(mk, c1);
+  const T vhat = A::div(vk, c2);
+  const T xk = x[k];
+  const T upd = A::add(A::div(mhat, A::add(A::sqrt(vhat), T(u.eps))), A::mul(T(u.wd), xk));
+  const double xd = double(xk), ud = double(upd);
+  sx = __dadd_rn(sx, __dmul_rn(xd, xd));
+  su = __dadd_rn(su, __dmul_rn(ud, ud));
+}
+
+// Pass 1 over ALL selected groups in one launch: one warp per chunk (the same
+// chunk decomposition as the fused TMA kernel's work list), the chunk's
+// (||x||^2, ||update||^2) partial reduced by a fixed xor tree and stored at
+// its chunk index, so the result does not depend on scheduling.
 template <typename T>
 __global__ void __launch_bounds__(kLT) lamb_pass1_kernel(const T* __restrict__ x, T* __restrict__ g,
                                                          const T* __restrict__ grad, T* __restrict__ m,
-                                                         T* __restrict__ v, uint64_t off, uint64_t len,
-                                                         ScalarSet ss, Uniform u, double* __restrict__ partial) {
-  using A = LA<T>;
-  const T c1 = T(ss.c1), c2 = T(ss.c2), b1 = T(u.b1), b2 = T(u.b2), omb1 = T(u.one_m_b1), omb2 = T(u.one_m_b2),
-          eps = T(u.eps), wd = T(u.wd);
-  double sx = 0.0, su = 0.0;
-  for (uint64_t i = blockIdx.x * uint64_t(kLT) + threadIdx.x; i < len; i += uint64_t(gridDim.x) * kLT) {
-    const uint64_t k = off + i;
-    const T gd = grad ? grad[k] : g[k];
-    if (grad) g[k] = gd;  // block.g = grad (optim.cpp:349)
-    const T mk = A::add(A::mul(b1, m[k]), A::mul(omb1, gd));
-    const T vk = A::add(A::mul(b2, v[k]), A::mul(A::mul(omb2, gd), gd));
-    m[k] = mk;
-    v[k] = vk;
-    const T mhat = A::div(mk, c1);
-    const T vhat = A::div(vk, c2);
-    const T xk = x[k];
-    const T upd = A::add(A::div(mhat, A::add(A::sqrt(vhat), eps)), A::mul(wd, xk));
-    const double xd = double(xk), ud = double(upd);
-    sx = __dadd_rn(sx, __dmul_rn(xd, xd));
-    su = __dadd_rn(su, __dmul_rn(ud, ud));
-  }
-  __shared__ double shx[kLT], shu[kLT];
-  shx[threadIdx.x] = sx;
-  shu[threadIdx.x] = su;
-  __syncthreads();
-  for (int s = kLT / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
-      shx[threadIdx.x] = __dadd_rn(shx[threadIdx.x], shx[threadIdx.x + s]);
-      shu[threadIdx.x] = __dadd_rn(shu[threadIdx.x], shu[threadIdx.x + s]);
+                                                         T* __restrict__ v, const WorkItem* __restrict__ work,
+                                                         uint32_t n_work, uint32_t total_chunks, uint32_t chunk_elems,
+                                                         const ScalarSet* __restrict__ sets, Uniform u,
+                                                         double2* __restrict__ partial) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (kLT / 32);
+  for (uint32_t c = blockIdx.x * (kLT / 32) + (threadIdx.x >> 5); c < total_chunks; c += warps) {
+    uint32_t lo = 0, hi = n_work - 1;  // last item with chunk_begin <= c
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (work[mid].chunk_begin <= c) lo = mid;
+      else hi = mid - 1;
     }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    partial[2 * blockIdx.x] = shx[0];
-    partial[2 * blockIdx.x + 1] = shu[0];
+    const WorkItem w = work[lo];
+    const ScalarSet ss = sets[w.sidx];
+    const T c1 = T(ss.c1), c2 = T(ss.c2);
+    const uint64_t begin = w.off + uint64_t(c - w.chunk_begin) * chunk_elems;
+    const uint64_t end = min(begin + chunk_elems, w.off + w.len);
+    double sx = 0.0, su = 0.0;
+    for (uint64_t k = begin + lane; k < end; k += 32) lamb_elem<T>(x, g, grad, m, v, k, c1, c2, u, sx, su);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, o));
+      su = __dadd_rn(su, __shfl_xor_sync(0xffffffffu, su, o));
+    }
+    if (lane == 0) partial[c] = make_double2(sx, su);
   }
 }
 
-// one CTA: fixed-order tree over the pass-1 partials -> trust ratio
-__global__ void __launch_bounds__(kLT) lamb_trust_kernel(const double* __restrict__ partial, int nparts, double eta,
-                                                         double wd, double* __restrict__ trust_out,
-                                                         ScalarSet* __restrict__ set) {
+// One CTA per group: fixed-order reduction of its chunk partials -> trust
+// ratio (optim.cpp:288-290), saved (:294) and folded into the group's
+// ScalarSet as scaled = eta * trust for the x pass (:292).
+__global__ void __launch_bounds__(kLT) lamb_trust_kernel(const WorkItem* __restrict__ work,
+                                                         const double2* __restrict__ partial, double wd,
+                                                         double* __restrict__ trust_table, uint32_t depth,
+                                                         ScalarSet* __restrict__ sets) {
+  const WorkItem w = work[blockIdx.x];
   __shared__ double shx[kLT], shu[kLT];
   double sx = 0.0, su = 0.0;
-  for (int i = threadIdx.x; i < nparts; i += kLT) {
-    sx = __dadd_rn(sx, partial[2 * i]);
-    su = __dadd_rn(su, partial[2 * i + 1]);
+  for (uint32_t i = threadIdx.x; i < w.nchunks; i += kLT) {
+    const double2 p = partial[w.chunk_begin + i];
+    sx = __dadd_rn(sx, p.x);
+    su = __dadd_rn(su, p.y);
   }
   shx[threadIdx.x] = sx;
   shu[threadIdx.x] = su;
@@ -103,33 +137,35 @@ __global__ void __launch_bounds__(kLT) lamb_trust_kernel(const double* __restric
   if (threadIdx.x == 0) {
     const double xn = __dsqrt_rn(shx[0]), un = __dsqrt_rn(shu[0]);
     const double trust = (xn > 0.0 && un > 0.0) ? __ddiv_rn(xn, un) : 1.0;  // optim.cpp:290
-    *trust_out = trust;
-    set->eta = __dmul_rn(eta, trust);  // (eta * trust) * update, optim.cpp:292
+    trust_table[uint64_t(w.gid) * depth + w.pad] = trust;
+    ScalarSet* set = sets + w.sidx;
+    set->eta = __dmul_rn(set->eta, trust);  // (eta * trust) * update
     set->denom = __dsub_rn(1.0, __dmul_rn(set->eta, wd));
   }
 }
 
 }  // namespace
 
-int lamb_parts_for(uint64_t len) {
-  uint64_t b = (len + kLT * 16 - 1) / (kLT * 16);
-  return static_cast<int>(b < 1 ? 1 : (b > 1184 ? 1184 : b));
-}
-
-int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, uint64_t off, uint64_t len,
-                      const ScalarSet& ss, const Uniform& u, double* partial, double* trust_out,
-                      ScalarSet* set_dev, void* stream) {
+int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, const WorkItem* work,
+                      uint32_t n_work, uint32_t total_chunks, uint32_t chunk_elems, ScalarSet* sets,
+                      const Uniform& u, double* partial, double* trust_table, uint32_t depth, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
-  const int parts = lamb_parts_for(len);
+  if (n_work == 0 || total_chunks == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t want = (total_chunks + kLT / 32 - 1) / (kLT / 32);
+  const uint32_t grid = want < uint32_t(sms) * 8 ? want : uint32_t(sms) * 8;
+  auto* p2 = reinterpret_cast<double2*>(partial);
   if (dtype == RW_F64)
-    lamb_pass1_kernel<double><<<parts, kLT, 0, st>>>(static_cast<const double*>(x), static_cast<double*>(g),
-                                                     static_cast<const double*>(grad), static_cast<double*>(m),
-                                                     static_cast<double*>(v), off, len, ss, u, partial);
+    lamb_pass1_kernel<double><<<grid, kLT, 0, st>>>(
+        static_cast<const double*>(x), static_cast<double*>(g), static_cast<const double*>(grad),
+        static_cast<double*>(m), static_cast<double*>(v), work, n_work, total_chunks, chunk_elems, sets, u, p2);
   else
-    lamb_pass1_kernel<float><<<parts, kLT, 0, st>>>(static_cast<const float*>(x), static_cast<float*>(g),
-                                                    static_cast<const float*>(grad), static_cast<float*>(m),
-                                                    static_cast<float*>(v), off, len, ss, u, partial);
-  lamb_trust_kernel<<<1, kLT, 0, st>>>(partial, parts, ss.eta, u.wd, trust_out, set_dev);
+    lamb_pass1_kernel<float><<<grid, kLT, 0, st>>>(
+        static_cast<const float*>(x), static_cast<float*>(g), static_cast<const float*>(grad),
+        static_cast<float*>(m), static_cast<float*>(v), work, n_work, total_chunks, chunk_elems, sets, u, p2);
+  lamb_trust_kernel<<<n_work, kLT, 0, st>>>(work, p2, u.wd, trust_table, depth, sets);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -110,9 +110,14 @@ struct rw_state {
   // ring of the last kTrustDepth trust ratios, written by lamb_trust_kernel;
   // head/count are host-side so the stack top is known without a sync.
   double* d_trust = nullptr;       // [G * kTrustDepth]
-  double* d_partial = nullptr;     // pass-1 scratch, 2 doubles per CTA
+  double* d_partial = nullptr;     // pass-1 scratch, 2 doubles per chunk
+  uint64_t partial_cap = 0;
   std::vector<uint64_t> trust_head;
   std::vector<uint32_t> trust_count;
+  // host-resident undo pipeline (rw_optimizer_undo_host)
+  cudaStream_t h2d = nullptr;
+  cudaStream_t d2h = nullptr;
+  std::vector<cudaEvent_t> evs;
 };
 
 namespace {
@@ -213,7 +218,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     w.chunk_begin = static_cast<uint32_t>(chunk);
     w.sidx = lamb ? i : set_of[undo ? gr.t : gr.t + 1];
     w.flags = (copy_only && copy_only[i]) ? rwb::kWorkCopyOnly : 0u;
-    w.pad = 0;
+    w.pad = lamb && !undo ? static_cast<uint32_t>(s->trust_head[ids[i]] % kTrustDepth) : 0u;  // trust slot
     chunk += w.nchunks;
   }
   if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one call");
@@ -224,16 +229,17 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * n_sets,
                             cudaMemcpyHostToDevice, cs));
     if (lamb && !undo) {
-      // step_lamb first pass per group: m, v, both norms, trust -> d_sets[i]
-      const rwb::Uniform u = uniform_of(h);
-      for (uint32_t i = 0; i < n; ++i) {
-        const rw_group& gr = s->mirror[ids[i]];
-        const uint64_t slot = s->trust_head[ids[i]] % kTrustDepth;
-        int e = rwb::launch_lamb_pass1(s->dtype, s->x, s->g, grad == s->g ? nullptr : grad, s->m, s->v, gr.offset,
-                                       gr.len, sl.h_sets[i], u, s->d_partial,
-                                       s->d_trust + uint64_t(ids[i]) * kTrustDepth + slot, sl.d_sets + i, stream);
-        if (e) return cuda_fail(static_cast<cudaError_t>(e), "lamb pass 1");
+      // step_lamb first pass over every group: m, v, both norms, trust
+      if (s->partial_cap < chunk) {
+        cudaFree(s->d_partial);
+        s->d_partial = nullptr;
+        RW_CUDA(cudaMalloc(&s->d_partial, sizeof(double) * 2 * chunk));
+        s->partial_cap = chunk;
       }
+      int e = rwb::launch_lamb_pass1(s->dtype, s->x, s->g, grad == s->g ? nullptr : grad, s->m, s->v, sl.d_work,
+                                     n_items, static_cast<uint32_t>(chunk), ce, sl.d_sets, uniform_of(h),
+                                     s->d_partial, s->d_trust, kTrustDepth, stream);
+      if (e) return cuda_fail(static_cast<cudaError_t>(e), "lamb pass 1");
       grad = nullptr;  // pass 1 cached it in g
     }
     rwb::LaunchArgs a;
@@ -404,7 +410,6 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
   if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_groups, sizeof(rw_group) * n_groups);
   if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_trust, sizeof(double) * n_groups * kTrustDepth);
   if (e == cudaSuccess && n_groups) e = cudaMemset(s->d_trust, 0, sizeof(double) * n_groups * kTrustDepth);
-  if (e == cudaSuccess && n_groups) e = cudaMalloc(&s->d_partial, sizeof(double) * 2 * 4096);
   if (e == cudaSuccess && n_groups)
     e = cudaMemcpy(s->d_groups, s->mirror.data(), sizeof(rw_group) * n_groups, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
@@ -432,6 +437,9 @@ void rw_state_destroy(rw_state* s) {
   cudaFree(s->d_groups);
   cudaFree(s->d_trust);
   cudaFree(s->d_partial);
+  if (s->h2d) cudaStreamSynchronize(s->h2d), cudaStreamDestroy(s->h2d);
+  if (s->d2h) cudaStreamSynchronize(s->d2h), cudaStreamDestroy(s->d2h);
+  for (cudaEvent_t e : s->evs) cudaEventDestroy(e);
   delete s;
 }
 
@@ -583,10 +591,16 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint3
   return launch_groups(s, h, ids, n, false, grad, etas, stream);
 }
 
-// optimizer_undo, optim.cpp:366-385 and the per-kind guards of undo_<kind>
-int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, void* stream) {
+}  // extern "C"
+
+namespace {
+// The guards of optimizer_undo (optim.cpp:366-385) and of undo_<kind>, for
+// every group, before anything is launched; fills the per-group eta (LAMB:
+// eta * saved trust ratio).
+int undo_prepare(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, std::vector<double>& etas,
+                 void* stream) {
   if (!s || !h || (n && !ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
-  std::vector<double> etas(n);
+  etas.assign(n, 0.0);
   std::vector<uint8_t> seen(s->mirror.size(), 0);
   for (uint32_t i = 0; i < n; ++i) {
     if (ids[i] >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", ids[i]);
@@ -628,11 +642,175 @@ int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint3
   if ((h->kind != RW_SGD && !s->m) ||
       ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB) && !s->v))
     return fail(RW_INVALID_ARGUMENT, "%s needs m/v buffers", kind_name(h->kind));
-  if (h->kind == RW_LAMB) {
-    int st = lamb_undo_scalars(s, h, ids, n, etas, stream);
-    if (st) return st;
-  }
+  if (h->kind == RW_LAMB) return lamb_undo_scalars(s, h, ids, n, etas, stream);
+  return RW_OK;
+}
+}  // namespace
+
+extern "C" {
+
+// optimizer_undo, optim.cpp:366-385 and the per-kind guards of undo_<kind>
+int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, void* stream) {
+  std::vector<double> etas;
+  int st = undo_prepare(s, h, ids, n, etas, stream);
+  if (st) return st;
   return launch_groups(s, h, ids, n, true, nullptr, etas, stream);
+}
+
+// optimizer_undo over a state whose bytes live in HOST memory (same flat
+// layout): the device buffers of `s` are the staging area.  The groups are
+// cut into slices of ~slice_elems elements in layout order; slice k's H2D
+// (copy stream 1), undo (the caller's stream) and D2H (copy stream 2) run as a
+// three-stage pipeline, so the two PCIe directions and the kernel overlap.
+int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, const void* hx,
+                           const void* hg, const void* hm, const void* hv, void* ox, void* om, void* ov,
+                           uint64_t slice_elems, void* stream) {
+  std::vector<double> etas;
+  int st = undo_prepare(s, h, ids, n, etas, stream);
+  if (st) return st;
+  const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB;
+  if (!hx || !hg || !ox || (um && (!hm || !om)) || (uv && (!hv || !ov)))
+    return fail(RW_INVALID_ARGUMENT, "host x, g (and m, v as the kind needs) in and out buffers required");
+  if (n == 0) return RW_OK;
+  if (slice_elems == 0) slice_elems = 16ull << 20;
+  RW_CUDA(cudaSetDevice(s->device));
+  auto cs = static_cast<cudaStream_t>(stream);
+  if (!s->h2d) RW_CUDA(cudaStreamCreateWithFlags(&s->h2d, cudaStreamNonBlocking));
+  if (!s->d2h) RW_CUDA(cudaStreamCreateWithFlags(&s->d2h, cudaStreamNonBlocking));
+  // groups in layout order -> slices
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(),
+            [&](uint32_t a, uint32_t b) { return s->mirror[ids[a]].offset < s->mirror[ids[b]].offset; });
+  struct SliceDesc {
+    uint64_t begin, end;
+    std::vector<uint32_t> gids;
+    std::vector<double> etas;
+  };
+  std::vector<SliceDesc> slices;
+  for (uint32_t k : order) {
+    const rw_group& gr = s->mirror[ids[k]];
+    if (slices.empty() || slices.back().end - slices.back().begin >= slice_elems) {
+      // slices tile the span contiguously: unselected groups inside it pass through
+      const uint64_t b = slices.empty() ? gr.offset : slices.back().end;
+      slices.push_back(SliceDesc{b, b, {}, {}});
+    }
+    SliceDesc& sd = slices.back();
+    sd.end = std::max<uint64_t>(sd.end, gr.offset + gr.len);
+    sd.gids.push_back(ids[k]);
+    sd.etas.push_back(etas[k]);
+  }
+  while (s->evs.size() < 3 * slices.size() + 1) {
+    cudaEvent_t e;
+    RW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    s->evs.push_back(e);
+  }
+  // One work list for every slice, uploaded before the first bulk H2D so no
+  // small metadata copy queues behind the slice copies on the H2D engine.
+  // Each slice's items are contiguous, their chunk_begin relative to it.
+  Slot& sl = s->slots[s->next_slot];
+  s->next_slot = (s->next_slot + 1) % kSlots;
+  const bool lamb = h->kind == RW_LAMB;
+  std::map<uint64_t, uint32_t> set_of;
+  for (uint32_t i = 0; i < n; ++i) set_of.emplace(s->mirror[ids[i]].t, 0);
+  const uint32_t n_sets = lamb ? n : static_cast<uint32_t>(set_of.size());
+  st = ensure_slot(s, sl, n, n_sets);
+  if (st) return st;
+  {
+    uint32_t k = 0;
+    for (auto& kv : set_of) kv.second = k++;
+  }
+  const uint32_t ce = rwb::chunk_elems_for(s->dtype);
+  std::vector<uint32_t> first(slices.size()), chunks(slices.size());
+  uint32_t item = 0;
+  for (size_t k = 0; k < slices.size(); ++k) {
+    first[k] = item;
+    uint64_t chunk = 0;
+    for (size_t j = 0; j < slices[k].gids.size(); ++j) {
+      const uint32_t gid = slices[k].gids[j];
+      const rw_group& gr = s->mirror[gid];
+      const uint32_t sidx = lamb ? item : set_of[gr.t];
+      sl.h_sets[sidx] = scalars_at(h, gr.t, slices[k].etas[j]);
+      rwb::WorkItem& w = sl.h_work[item++];
+      w.off = gr.offset;
+      w.len = gr.len;
+      w.new_t = gr.t - 1;
+      w.gid = gid;
+      w.nchunks = static_cast<uint32_t>((gr.len + ce - 1) / ce);
+      w.chunk_begin = static_cast<uint32_t>(chunk);
+      w.sidx = sidx;
+      w.flags = 0;
+      w.pad = 0;
+      chunk += w.nchunks;
+    }
+    if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one slice");
+    chunks[k] = static_cast<uint32_t>(chunk);
+  }
+  RW_CUDA(cudaMemcpyAsync(sl.d_work, sl.h_work, sizeof(rwb::WorkItem) * n, cudaMemcpyHostToDevice, cs));
+  RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * n_sets, cudaMemcpyHostToDevice, cs));
+  const size_t es = elem_size(s->dtype);
+  cudaEvent_t start = s->evs[3 * slices.size()];
+  RW_CUDA(cudaEventRecord(start, cs));  // prior work + the metadata upload first
+  RW_CUDA(cudaStreamWaitEvent(s->h2d, start, 0));
+  RW_CUDA(cudaStreamWaitEvent(s->d2h, start, 0));
+  const void* hin[4] = {hx, hg, um ? hm : nullptr, uv ? hv : nullptr};
+  void* din[4] = {s->x, s->g, s->m, s->v};
+  void* hout[3] = {ox, um ? om : nullptr, uv ? ov : nullptr};
+  void* dout[3] = {s->x, s->m, s->v};
+  for (size_t k = 0; k < slices.size(); ++k) {
+    const SliceDesc& sd = slices[k];
+    const uint64_t off = sd.begin * es, bytes = (sd.end - sd.begin) * es;
+    for (int b = 0; b < 4; ++b)
+      if (hin[b])
+        RW_CUDA(cudaMemcpyAsync(static_cast<char*>(din[b]) + off, static_cast<const char*>(hin[b]) + off, bytes,
+                                cudaMemcpyHostToDevice, s->h2d));
+    RW_CUDA(cudaEventRecord(s->evs[3 * k], s->h2d));
+    RW_CUDA(cudaStreamWaitEvent(cs, s->evs[3 * k], 0));
+    rwb::LaunchArgs a;
+    a.dtype = s->dtype;
+    a.kind = h->kind;
+    a.undo = true;
+    a.x = s->x;
+    a.g = s->g;
+    a.m = s->m;
+    a.v = s->v;
+    a.vmax = s->vmax;
+    a.grad = nullptr;
+    a.work = sl.d_work + first[k];
+    a.n_work = static_cast<uint32_t>(sd.gids.size());
+    a.total_chunks = chunks[k];
+    a.chunk_elems = ce;
+    a.sets = sl.d_sets;
+    a.u = uniform_of(h);
+    a.groups = s->d_groups;
+    a.done = sl.d_done + first[k];
+    int e = rwb::launch_optim(a, stream);
+    if (e) {
+      cudaStreamSynchronize(s->h2d);
+      return cuda_fail(static_cast<cudaError_t>(e), "optim kernel launch");
+    }
+    RW_CUDA(cudaEventRecord(s->evs[3 * k + 1], cs));
+    RW_CUDA(cudaStreamWaitEvent(s->d2h, s->evs[3 * k + 1], 0));
+    for (int b = 0; b < 3; ++b)
+      if (hout[b])
+        RW_CUDA(cudaMemcpyAsync(static_cast<char*>(hout[b]) + off, static_cast<const char*>(dout[b]) + off, bytes,
+                                cudaMemcpyDeviceToHost, s->d2h));
+    RW_CUDA(cudaEventRecord(s->evs[3 * k + 2], s->d2h));
+  }
+  for (uint32_t i = 0; i < n; ++i) {  // host mirror follows the kernels' marker writes
+    rw_group& gr = s->mirror[ids[i]];
+    gr.t -= 1;
+    gr.updated = 0;
+    if (lamb) {
+      s->trust_head[ids[i]] -= 1;
+      s->trust_count[ids[i]] -= 1;
+    }
+  }
+  // the call is ordered on `stream`: it completes when the last D2H lands
+  RW_CUDA(cudaStreamWaitEvent(cs, s->evs[3 * (slices.size() - 1) + 2], 0));
+  RW_CUDA(cudaEventRecord(sl.ev, cs));
+  sl.used = true;
+  return RW_OK;
 }
 
 // ---------------- numerics ----------------

@@ -193,6 +193,23 @@ class DeviceState:
         check(LIB.rw_optimizer_undo(self._h, C.byref(hyper.to_c()), arr, len(ids),
                                     C.c_void_p(_stream_handle(stream))))
 
+    def undo_from_host(self, hyper: OptimizerHyper, host: dict, out: dict | None = None,
+                       ids: Iterable[int] | None = None, slice_elems: int = 0, stream=None) -> None:
+        """optimizer_undo of a state held in (pinned) host tensors host["x"/"g"/"m"/"v"]
+        (this state's flat layout); results into out[...] (default: in place).
+        H2D, undo and D2H are pipelined per slice of groups (rw_optimizer_undo_host)."""
+        ids = self.update_order() if ids is None else list(ids)
+        arr = (C.c_uint32 * max(len(ids), 1))(*ids)
+        out = host if out is None else out
+        for k, t in list(host.items()) + list(out.items()):
+            if t is not None and (t.numel() < self.total or t.dtype != self.dtype or t.is_cuda):
+                raise RwError(2, f"ShapeMismatch: host buffer {k} must be a {self.dtype} CPU tensor of "
+                                 f">= {self.total} elements")
+        p = lambda d, k: C.c_void_p(d[k].data_ptr()) if d.get(k) is not None else None  # noqa: E731
+        check(LIB.rw_optimizer_undo_host(self._h, C.byref(hyper.to_c()), arr, len(ids), p(host, "x"),
+                                         p(host, "g"), p(host, "m"), p(host, "v"), p(out, "x"), p(out, "m"),
+                                         p(out, "v"), int(slice_elems), C.c_void_p(_stream_handle(stream))))
+
     def check_finite(self, stream=None) -> None:
         """Raise NumericalError if the last step/undo produced a non-finite value."""
         check(LIB.rw_state_check(self._h, C.c_void_p(_stream_handle(stream))))

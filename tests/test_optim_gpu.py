@@ -272,3 +272,36 @@ def test_large_state_roundtrip_sampled(restate):
     # fp32 round trip: x within 1 ulp of max(|x_t|, |x_t+1|)
     sp = torch.maximum(x0.abs(), xs.abs())
     assert ((st.x - x0).abs() <= 2 * torch.finfo(torch.float32).eps * sp + 1e-30).all()
+
+
+@pytest.mark.parametrize("kind", [ADAM, SGDM])
+def test_undo_from_host_pipelined_equals_device_undo(kind):
+    """rw_optimizer_undo_host (H2D | undo | D2H pipelined per slice) gives the
+    same bits and markers as the device-resident undo, for many small slices."""
+    sizes = [1000, 77, 5000, 64, 3000, 12345]
+    h = HYP[kind]
+    ref = DeviceState(sizes, dtype=torch.float32, kind=kind)
+    seeded_fill_(ref.x, 1)
+    seeded_fill_(ref.g, 2)
+    seeded_fill_(ref.m, 3)
+    if ref.v is not None:
+        seeded_fill_(ref.v, 4)
+        ref.v.abs_()
+    ref.write_markers([(5, 1)] * len(sizes))
+    host = {k: getattr(ref, k).cpu().pin_memory() for k in ("x", "g", "m", "v") if getattr(ref, k) is not None}
+    st = DeviceState(sizes, dtype=torch.float32, kind=kind)
+    st.write_markers([(5, 1)] * len(sizes))
+    out = {k: torch.zeros_like(v).pin_memory() for k, v in host.items() if k != "g"}
+    ids = [5, 3, 1, 0]
+    st.undo_from_host(h, host, out, ids=ids, slice_elems=2000)
+    torch.cuda.synchronize()
+    ref.undo(h, ids)
+    lo, hi = st.offsets[0], st.offsets[5] + sizes[5]  # the span first..last selected group
+    for k in out:
+        # undone groups: bit-exact vs device undo; groups 2, 4 pass through unchanged
+        assert torch.equal(out[k][lo:hi].cuda(), getattr(ref, k)[lo:hi]), k
+        assert torch.equal(getattr(st, k)[lo:hi], getattr(ref, k)[lo:hi]), k
+    assert st.markers() == ref.markers()
+    with pytest.raises(RwError) as e:  # guards before any copy
+        st.undo_from_host(h, host, out, ids=[0])
+    assert e.value.name == "NothingToUndo"
