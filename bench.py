@@ -108,8 +108,9 @@ def _peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return dict(hbm_gbs=d.get("hbm_gbs", 6650.0), src="measured")
-    return dict(hbm_gbs=6650.0, src="fallback")
+        return dict(hbm_gbs=d.get("hbm_gbs", 6650.0), bf16_sustained=d.get("bf16_tflops_sustained", 1382.3),
+                    src="measured")
+    return dict(hbm_gbs=6650.0, bf16_sustained=1382.3, src="fallback")
 
 
 def _ncu_traffic(kernel_key: str):
@@ -522,7 +523,8 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
                          f"{m} micro-batches x {rows} rows, logs in HBM, parallel recovery over {world} GPU(s)",
                 iterations=iters, ms_per_iteration=round(ms_max / iters, 3),
                 tflops_aggregate=round(tflops, 1), tflop_per_iteration=round(flop_mb * m / 1e12, 2),
-                frac_of_bf16_peak_aggregate=round(tflops / (1649.8 * world), 4),
+                frac_of_bf16_sustained_aggregate=round(tflops / (_peaks().get("bf16_sustained", 1382.3) * world), 4),
+                frac_of_bf16_burst_aggregate=round(tflops / (1649.8 * world), 4),
                 gemm="tcgen05 kind::f16 M128xN256xK16, TMA SW128, TMEM double-buffered accumulators")
 
 

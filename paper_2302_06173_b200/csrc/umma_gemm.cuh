@@ -490,6 +490,13 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
       : "memory");
 }
 
+#ifdef RWB_PAIR_EXPERIMENT
+// tools/gemm_test.cu instrumentation of the parked pair kernel (per CTA):
+// [0] MMA-warp cycles waiting on full_bar, [1] on tempty_bar, [2] total MMA
+// loop cycles, [3] producer cycles waiting on empty_bar
+__device__ long long g_pair_dbg[148][4];
+#endif
+
 template <int BN>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;
@@ -526,7 +533,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tma_a);
     prefetch_tmap(&tma_b);
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full_bar[i], 2);  // leader: its expect_tx arrive + the peer's arrive
+      mbar_init(&full_bar[i], 1);  // the leader's expect_tx arrive (bytes of BOTH CTAs' loads)
       mbar_init(&empty_bar[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -557,12 +564,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int m0 = tm * PM + int(rank) * BM;     // this CTA's A rows
         const int nb0 = tn * BN + int(rank) * BNH;   // this CTA's half of B
         for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef RWB_PAIR_EXPERIMENT
+          const long long w0 = clock64();
+#endif
           mbar_wait(&empty_bar[stage], phase ^ 1);
+#ifdef RWB_PAIR_EXPERIMENT
+          g_pair_dbg[blockIdx.x][3] += clock64() - w0;
+#endif
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
           const uint32_t fb = smem_u32(&full_bar[stage]);
+#if defined(RWB_PAIR_EXPERIMENT) && RWB_PAIR_EXPERIMENT == 2
+          // no data movement after the first fill: timing of MMA + sync only
+          if (tile != cid || kb >= S) {
+            if (leader) mbar_arrive(&full_bar[stage]);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+#endif
+          // only the leader arrives (with both CTAs' byte count); the peer's
+          // TMA completes its bytes on the leader's barrier directly
           if (leader) mbar_expect_tx(&full_bar[stage], 2 * C::kStageBytes);
-          else mbar_arrive_cluster(mapa_rank0(fb));
           const uint32_t lbar = fb & 0xFEFFFFFFu;  // the leader's barrier
           const int k0 = kb * BK;
           if constexpr (AMAJ == K_MAJOR) {
@@ -592,12 +617,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+#ifdef RWB_PAIR_EXPERIMENT
+      const long long l0 = clock64();
+#endif
       for (int tile = cid; tile < num_tiles; tile += ncl) {
+#ifdef RWB_PAIR_EXPERIMENT
+        const long long a0 = clock64();
+#endif
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+#ifdef RWB_PAIR_EXPERIMENT
+        if (lane == 0) g_pair_dbg[blockIdx.x][1] += clock64() - a0;
+#endif
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef RWB_PAIR_EXPERIMENT
+          const long long f0 = clock64();
+#endif
           mbar_wait(&full_bar[stage], phase);
+#ifdef RWB_PAIR_EXPERIMENT
+          if (lane == 0) g_pair_dbg[blockIdx.x][0] += clock64() - f0;
+#endif
           tc_fence_after();
           if (lane == 0) {
             const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
@@ -625,6 +665,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           acc_phase ^= 1;
         }
       }
+#ifdef RWB_PAIR_EXPERIMENT
+      if (lane == 0) g_pair_dbg[blockIdx.x][2] += clock64() - l0;
+#endif
     }
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue (both CTAs, own 128 rows) =====================
