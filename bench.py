@@ -417,7 +417,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     if rank == 0:
         _fill_adam_state(st)
     out = {}
-    modes = ["nccl", "fused", "auto"] if world > 1 else ["local"]
+    modes = ["nccl", "scatter_allgather", "fused", "auto"] if world > 1 else ["local"]
     for mode in modes:
         res = []
         kinfo = []
@@ -431,8 +431,8 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
             t_wall = time.perf_counter()
             plan = resolve(st.markers() if rank == 0 else [], h, lens=sizes if rank == 0 else None,
                            device=device)
-            if mode == "auto":
-                used, nbytes = recover(st, h, plan, src=0)
+            if mode in ("auto", "scatter_allgather"):
+                used, nbytes = recover(st, h, plan, src=0, transfer=mode)
                 kinfo.append({"used": used})
             elif mode == "fused":
                 nbytes = recover_replication_fused(st, h, plan, src=0)

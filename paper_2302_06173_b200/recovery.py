@@ -238,9 +238,43 @@ def _broadcast_saved_scalars(state, src: int, group=None) -> None:
             state.set_saved_scalars(i, rows[i, 1:1 + c].tolist())
 
 
-def recover_replication(state, src: int, include_grad: bool = False, group=None) -> int:
-    """recover_replication: broadcast the resolved state from the
-    surviving rank `src` to every other rank of `group` (NCCL over NVLink).
+def _scatter_allgather(buf: torch.Tensor, src: int, group=None) -> None:
+    """Broadcast of `buf` from `src` as scatter + all-gather: the source hands
+    slice r to rank r (its egress carries the state once), then every rank
+    all-gathers the slices (in place; NCCL uses NVLS on NVSwitch), so each
+    rank's ingress carries the state once and no single link is serialised
+    over the replacements."""
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    n = buf.numel()
+    chunk = n // world
+    main = chunk * world
+    if chunk:
+        views = [buf[r * chunk:(r + 1) * chunk] for r in range(world)]
+        glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)  # noqa: E731
+        if rank == src:
+            ops = [dist.P2POp(dist.isend, views[r], glob(r), group) for r in range(world) if r != src]
+        else:
+            ops = [dist.P2POp(dist.irecv, views[rank], glob(src), group)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        if dist.get_backend(group) == "nccl":
+            dist.all_gather_into_tensor(buf[:main], views[rank], group=group)
+        else:  # gloo: list form
+            parts = [torch.empty_like(views[rank]) for _ in range(world)]
+            dist.all_gather(parts, views[rank].clone(), group=group)
+            for r in range(world):
+                if r != rank:
+                    views[r].copy_(parts[r])
+    if main < n:  # the tail (< world elements)
+        dist.broadcast(buf[main:], src=glob(src) if chunk else src, group=group)
+
+
+def recover_replication(state, src: int, include_grad: bool = False, group=None,
+                        algo: str = "broadcast") -> int:
+    """recover_replication: copy the resolved state from the
+    surviving rank `src` to every other rank of `group` (NCCL over NVLink):
+    algo "broadcast" (ncclBroadcast ring) or "scatter_allgather" (each link
+    carries the state once; the better choice for several replacements).
     Bit-exact copy semantics; markers travel with it.  Returns bytes received
     per replacement."""
     if not (dist.is_available() and dist.is_initialized()):
@@ -248,7 +282,10 @@ def recover_replication(state, src: int, include_grad: bool = False, group=None)
     bufs = [state.x] + ([state.g] if include_grad else [])
     bufs += [b for b in (state.m, state.v) if b is not None]
     for b in bufs:
-        dist.broadcast(b, src=src, group=group)
+        if algo == "scatter_allgather":
+            _scatter_allgather(b, src, group)
+        else:
+            dist.broadcast(b, src=src, group=group)
     _broadcast_saved_scalars(state, src, group)
     mk = state.markers()
     backend = dist.get_backend(group)
@@ -265,16 +302,18 @@ def recover(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = Fals
     """apply_undo + recover_replication with the transfer picked per topology:
     one replacement -> the fused undo + NVLink push kernel (the survivor's
     egress feeds exactly one ingress, so the push runs at link speed and hides
-    the undo); several -> undo, then NCCL's pipelined ring broadcast (a single
+    the undo); several -> undo, then scatter + all-gather over NCCL (a single
     pusher would serialise its egress over the replacements).  The fused path
-    needs every rank on one node (CUDA IPC).  Returns (transfer used, bytes
-    per replacement)."""
+    needs every rank on one node (CUDA IPC).  transfer: "auto", "fused",
+    "scatter_allgather" or "broadcast".  Returns (transfer used, bytes per
+    replacement)."""
     world = dist.get_world_size(group)
     if transfer == "auto":
         same_node = world <= torch.cuda.device_count()
-        transfer = "fused" if (world == 2 and same_node) else "nccl"
+        transfer = "fused" if (world == 2 and same_node) else "scatter_allgather"
     if transfer == "fused":
         return transfer, recover_replication_fused(state, hyper, plan, src, include_grad, group)
     if dist.get_rank(group) == src:
         apply_resolution(state, hyper, plan)
-    return "nccl", recover_replication(state, src, include_grad, group)
+    algo = "scatter_allgather" if transfer == "scatter_allgather" else "broadcast"
+    return transfer, recover_replication(state, src, include_grad, group, algo=algo)

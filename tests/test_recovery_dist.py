@@ -11,7 +11,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2302_06173_b200 import ADAM, AMSGRAD, OptimizerHyper
-from paper_2302_06173_b200.recovery import recover_replication, resolve
+from paper_2302_06173_b200.recovery import recover, recover_replication, resolve
 
 
 class HostState:
@@ -111,3 +111,28 @@ def test_resolver_two_survivors_world2():
     assert res[0]["blocked"] == "Undo"
     # AMSGrad cannot undo but every lagging group holds its gradient -> redo to 6
     assert res[0]["ams"] == ("Redo", 6) and res[1]["ams"] == ("Redo", 6)
+
+
+def scen_scatter_allgather(rank):
+    """N >= 3: one survivor, two replacements, scatter + all-gather transfer
+    (ragged length so the tail path runs too)."""
+    h = OptimizerHyper(kind=ADAM)
+    sizes = [5, 7, 11]
+    if rank == 0:
+        plan = resolve([(10, 0)] * 3, h, lens=sizes)
+        st = HostState(sizes, seed=9)
+        st.write_markers([(10, 0)] * 3)
+    else:
+        plan = resolve([], h)
+        st = HostState(sizes)
+    used, nbytes = recover(st, h, plan, src=0, transfer="scatter_allgather")
+    return dict(used=used, x=st.x.clone(), m=st.m.clone(), v=st.v.clone(), mk=st.markers(), nbytes=nbytes)
+
+
+def test_scatter_allgather_world3():
+    res = _run(scen_scatter_allgather, world=3)
+    for r in (1, 2):
+        for k in ("x", "m", "v"):
+            assert torch.equal(res[0][k].view(torch.int32), res[r][k].view(torch.int32))
+        assert res[r]["mk"] == [(10, 0)] * 3
+    assert all(res[r]["used"] == "scatter_allgather" for r in range(3))
