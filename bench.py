@@ -472,12 +472,13 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
 
 
 def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 16384, m: int = 8,
-                 dims=(4096, 16384, 4096)) -> dict:
-    """Config 4: logging-based replay of one failed pipeline stage (two
-    affine+tanh layers 4096 -> 16384 -> 4096, micro-batch 8 x 2048 tokens =
-    16384 rows, m = 8 micro-batches, Adam) from logged boundary activations /
-    gradients resident in HBM, spread over the `world` GPUs as parallel
-    recovery (helper h replays mb with mb mod d == h; ascending-mb merge).
+                 dims=(4096, 16384, 4096), n_stages: int = 8) -> dict:
+    """Config 4: logging-based replay of the failed machine's 8-stage group
+    (each stage two affine+tanh layers 4096 -> 16384 -> 4096),
+    micro-batch 8 x 2048 tokens = 16384 rows, m = 8 micro-batches, Adam, from
+    logged boundary activations / gradients resident in HBM, spread over the
+    `world` GPUs as parallel recovery (helper h replays mb with mb mod d == h
+    through all 8 stages; ascending-mb ordered merge; every rank steps).
     Times `iters` replayed iterations end to end (max over ranks)."""
     import torch
     import torch.distributed as dist
@@ -485,7 +486,7 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
     from paper_2302_06173_b200 import ADAM, OptimizerHyper
     from paper_2302_06173_b200.replay import BoundaryLog, Stage, recover_parallel, replay_group, synth_inputs
     h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
-    st = Stage(3, dims[0], dims[1], dims[2], 2, 2302, ADAM, device=device.index)
+    sts = [Stage(s, dims[0], dims[1], dims[2], 2, 2302, ADAM, device=device.index) for s in range(n_stages)]
     log = BoundaryLog()
     mine = [mb for mb in range(m) if mb % world == rank]
     for mb in mine:  # synthetic logged tensors for this helper's micro-batches
@@ -494,13 +495,16 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
         for it in range(iters + 1):
             log.acts[(it, mb)] = a
             log.grads[(it, mb)] = g
-    flop_mb = 2 * rows * (dims[0] * dims[1] + dims[1] * dims[2]) * 2 + 2 * rows * dims[1] * dims[2]
+    # per layer per micro-batch: forward 2RKN + wgrad 2RKN + dgrad 2RKN, except
+    # the group's very first layer (its input gradient is never needed)
+    layer = [2 * rows * dims[0] * dims[1], 2 * rows * dims[1] * dims[2]]
+    flop_it = m * (n_stages * 3 * sum(layer) - layer[0])
 
     def run(it0, it1):
         if world > 1:
-            return recover_parallel([st], log, it0, it1, rows, m, 2302, h, first=False, last=False,
+            return recover_parallel(sts, log, it0, it1, rows, m, 2302, h, first=False, last=False,
                                     dim=dims[0], rank=rank, d=world)
-        return replay_group([st], log, it0, it1, rows, m, 2302, h, first=False, last=False, dim=dims[0])
+        return replay_group(sts, log, it0, it1, rows, m, 2302, h, first=False, last=False, dim=dims[0])
 
     run(0, 1)  # warm-up (also JIT-free: TMA maps, smem attributes)
     torch.cuda.synchronize()
@@ -516,14 +520,17 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    tflops = flop_mb * m * iters / (ms_max * 1e-3) / 1e12
-    del st, log
+    tflops = flop_it * iters / (ms_max * 1e-3) / 1e12
+    del sts, log
     torch.cuda.empty_cache()
-    return dict(workload="config 4: replay of one failed stage (4096->16384->4096 affine+tanh, Adam), "
-                         f"{m} micro-batches x {rows} rows, logs in HBM, parallel recovery over {world} GPU(s)",
+    sus = _peaks().get("bf16_sustained", 1382.3)
+    return dict(workload=f"config 4: replay of the failed {n_stages}-stage group (each stage 4096->16384->4096 "
+                         f"affine+tanh, Adam; {n_stages * 134}M params), {m} micro-batches x {rows} rows, logs in "
+                         f"HBM, parallel recovery over {world} GPU(s)",
                 iterations=iters, ms_per_iteration=round(ms_max / iters, 3),
-                tflops_aggregate=round(tflops, 1), tflop_per_iteration=round(flop_mb * m / 1e12, 2),
-                frac_of_bf16_sustained_aggregate=round(tflops / (_peaks().get("bf16_sustained", 1382.3) * world), 4),
+                tflops_aggregate=round(tflops, 1), tflop_per_iteration=round(flop_it / 1e12, 2),
+                roofline_ms_per_iteration=round(flop_it / (sus * world * 1e12) * 1e3, 2),
+                frac_of_bf16_sustained_aggregate=round(tflops / (sus * world), 4),
                 frac_of_bf16_burst_aggregate=round(tflops / (1649.8 * world), 4),
                 gemm="tcgen05 kind::f16 M128xN256xK16, TMA SW128, TMEM double-buffered accumulators")
 

@@ -158,9 +158,25 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n, int a_major, int
          | (uint32_t(m >> 4) << 24);    // M / 16
 }
 
+// y operand of EPI_DTANH_BF16 for one full 32-column chunk of one row:
+// 4 x 128-bit loads, issued ahead of use so their latency overlaps the
+// accumulator wait / the previous chunk.
+struct YChunk {
+  uint4 q[4];
+};
+__device__ __forceinline__ void load_y_chunk(const EpiArgs& ep, int row, int col0, int M, int N, YChunk& y) {
+  if (row < M && col0 + 32 <= N) {
+    const uint4* p = reinterpret_cast<const uint4*>(ep.y + int64_t(row) * ep.ldy + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y.q[q] = __ldg(p + q);
+  }
+}
+
 // Epilogue of one 32-column TMEM chunk for one accumulator row (thread).
+// yk: the chunk's y already in registers (EPI_DTANH_BF16, full chunks).
 template <int EPI>
-__device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int N, const EpiArgs& ep) {
+__device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int N, const EpiArgs& ep,
+                                          const YChunk* yk = nullptr) {
     if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
       float* o = static_cast<float*>(ep.out) + int64_t(row) * ep.ldo + col0;
       if (col0 + 32 <= N) {
@@ -177,8 +193,9 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
           *reinterpret_cast<float4*>(o + j) = w;
         }
       } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j)
-          o[j] = EPI == EPI_F32_ACC ? __fadd_rn(o[j], v[j]) : v[j];
+#pragma unroll
+        for (int j = 0; j < 32; ++j)  // constant trip count: v stays in registers
+          if (col0 + j < N) o[j] = EPI == EPI_F32_ACC ? __fadd_rn(o[j], v[j]) : v[j];
       }
     } else {
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + int64_t(row) * ep.ldo + col0;
@@ -204,10 +221,10 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
       } else if constexpr (EPI == EPI_DTANH_BF16) {
         const __nv_bfloat16* yp = ep.y + int64_t(row) * ep.ldy + col0;
         float yv[32];
-        if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads
+        if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads (prefetched when yk)
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
-            const uint4 u = *reinterpret_cast<const uint4*>(yp + j);
+            const uint4 u = yk ? yk->q[j / 8] : *reinterpret_cast<const uint4*>(yp + j);
             const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -241,19 +258,36 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
           *reinterpret_cast<uint4*>(o + j) = pk;
         }
       } else {
-        for (int j = 0; j < 32 && col0 + j < N; ++j) o[j] = __float2bfloat16_rn(w[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < N) o[j] = __float2bfloat16_rn(w[j]);
       }
     }
 }
 
 // Drain one accumulator tile: this thread owns TMEM lane `row - m0`.
+// EPI_DTANH_BF16: y0 holds chunk 0's y (loaded before the accumulator wait);
+// chunk c+1's y is loaded before chunk c is processed.
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, int n0, int M, int N, const EpiArgs& ep) {
+__device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, int n0, int M, int N, const EpiArgs& ep,
+                                              const YChunk* y0 = nullptr) {
+  if constexpr (EPI == EPI_DTANH_BF16) {
+    YChunk cur = *y0, nxt;
 #pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    float v[32];
-    tmem_ld_32cols(tbase + uint32_t(c0), v);
-    if (row < M) epi_chunk<EPI>(v, row, n0 + c0, N, ep);
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      if (c0 + 32 < BN) load_y_chunk(ep, row, n0 + c0 + 32, M, N, nxt);
+      float v[32];
+      tmem_ld_32cols(tbase + uint32_t(c0), v);
+      if (row < M) epi_chunk<EPI>(v, row, n0 + c0, N, ep, &cur);
+      cur = nxt;
+    }
+  } else {
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      tmem_ld_32cols(tbase + uint32_t(c0), v);
+      if (row < M) epi_chunk<EPI>(v, row, n0 + c0, N, ep);
+    }
   }
 }
 
@@ -414,11 +448,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       int tm, tn;
       tile_coords(tile, tiles_m, tiles_n, kGroupM, tm, tn);
       const int m0 = tm * BM, n0 = tn * BN;
+      const int row = m0 + ew * 32 + lane;
+      YChunk y0;
+      if constexpr (EPI == EPI_DTANH_BF16) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
-      epilogue_tile<BN, EPI>(tbase, row, n0, M, N, ep);
+      epilogue_tile<BN, EPI>(tbase, row, n0, M, N, ep, &y0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -678,11 +714,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int tile = cid; tile < num_tiles; tile += ncl) {
       int tm, tn;
       tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
+      const int row = tm * PM + int(rank) * BM + ew * 32 + lane;
+      YChunk y0;
+      if constexpr (EPI == EPI_DTANH_BF16) load_y_chunk(ep, row, tn * BN, M, N, y0);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = tm * PM + int(rank) * BM + ew * 32 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
-      epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep);
+      epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);

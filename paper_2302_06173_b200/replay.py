@@ -139,8 +139,11 @@ class Stage:
             w = self.state.view("x", 2 * l)
             check(LIB.rw_cast_f32_to_bf16(_p(w), _p(self.w16[l]), w.numel(), _sh(stream)))
 
-    def new_acts(self, rows: int) -> list[torch.Tensor]:
-        return [torch.empty(rows, d, dtype=torch.bfloat16, device=self.device) for d in self.dims]
+    def new_acts(self, rows: int, x: torch.Tensor | None = None) -> list[torch.Tensor]:
+        """Activation cache of one micro-batch; acts[0] aliases the input `x`
+        when given (the stage only reads it), so no copy is made."""
+        first = [x] if x is not None else [torch.empty(rows, self.dims[0], dtype=torch.bfloat16, device=self.device)]
+        return first + [torch.empty(rows, d, dtype=torch.bfloat16, device=self.device) for d in self.dims[1:]]
 
     def _scr(self, rows: int):
         if rows not in self._scratch:
@@ -271,8 +274,7 @@ class Pipeline:
             x = synth_inputs(self.seed, it, mb, self.rows, self.dim, device=dev)
             all_acts = []
             for s, st in enumerate(self.stages):
-                acts = st.new_acts(self.rows)
-                acts[0].copy_(x)
+                acts = st.new_acts(self.rows, x)
                 if log_group and log is not None and s == log_group[0] and s > 0:
                     log.put("act", it, mb, x, sender=s - 1, receiver=s)
                 x = st.forward(acts)
@@ -311,8 +313,7 @@ def replay_group(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, 
                     raise RwError(14, f"MissingLogData: activation ({it}, {mb})")
             all_acts = []
             for st in stages:
-                acts = st.new_acts(rows)
-                acts[0].copy_(x)
+                acts = st.new_acts(rows, x)
                 x = st.forward(acts)
                 all_acts.append(acts)
             if last:
@@ -351,8 +352,7 @@ def helper_pass(stages: Sequence[Stage], log: BoundaryLog, it: int, mbs: Sequenc
                 raise RwError(14, f"MissingLogData: activation ({it}, {mb})")
         all_acts = []
         for st in stages:
-            acts = st.new_acts(rows)
-            acts[0].copy_(x)
+            acts = st.new_acts(rows, x)
             x = st.forward(acts)
             all_acts.append(acts)
         if last:
