@@ -290,6 +290,16 @@ int rw_stage_forward(const rw_stage_desc* st, int64_t rows, void* const* acts, v
 int rw_stage_backward(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
                       void* grad_out, float* const* dw, float* const* db, int32_t accumulate,
                       void* scratch_dz0, void* scratch_dz1, float* scratch_f32, void* stream);
+/* Same, for consecutive stages replayed on one GPU: grad_in_is_dz != 0 means
+ * grad_in already holds this stage's last-layer dz (produced by the next
+ * stage with prev_y); prev_y != NULL (the previous stage's output, i.e.
+ * acts[0]) makes grad_out the PREVIOUS stage's last-layer dz instead of the
+ * boundary gradient, computed from the bf16-rounded boundary gradient exactly
+ * as that stage's own dtanh would (bit-identical to the unfused pair). */
+int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
+                         int32_t grad_in_is_dz, void* grad_out, const void* prev_y, float* const* dw,
+                         float* const* db, int32_t accumulate, void* scratch_dz0, void* scratch_dz1,
+                         float* scratch_f32, void* stream);
 
 /* mse_loss (model.cpp:174-188): grad = 2/(n*micro_batches) * (pred - target)
  * (bf16 out); *loss (device double, may be NULL) = mean squared error.

@@ -90,6 +90,9 @@ int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, co
                        const void* y_prev, void* dst, void* stream);
 int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
                        int accumulate, void* stream);
+// first-layer dgrad of stage k fused with stage k-1's dz: bf16(dX) * (1 - y^2)
+int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
+                          const void* y_prev_stage, void* dz_prev_stage, void* stream);
 int replay_dtanh_first(const void* g, const void* y, void* dz, uint64_t n, void* stream);
 int replay_colsum(const void* dz, int64_t rows, int64_t cols, float* db, float* scratch, int accumulate,
                   void* stream);

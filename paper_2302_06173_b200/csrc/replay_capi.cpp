@@ -50,18 +50,32 @@ int rw_stage_forward(const rw_stage_desc* st, int64_t rows, void* const* acts, v
 int rw_stage_backward(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
                       void* grad_out, float* const* dw, float* const* db, int32_t accumulate, void* dz0, void* dz1,
                       float* scratch, void* stream) {
+  return rw_stage_backward_ex(st, rows, acts, grad_in, 0, grad_out, nullptr, dw, db, accumulate, dz0, dz1, scratch,
+                              stream);
+}
+
+int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
+                         int32_t grad_in_is_dz, void* grad_out, const void* prev_y, float* const* dw,
+                         float* const* db, int32_t accumulate, void* dz0, void* dz1, float* scratch, void* stream) {
   int s = check_desc(st, rows);
   if (s) return s;
   if (!acts || !grad_in || !dw || !db || !dz0 || !dz1 || !scratch)
     return rfail(RW_INVALID_ARGUMENT, "null argument");
+  if (prev_y && !grad_out) return rfail(RW_INVALID_ARGUMENT, "prev_y needs grad_out");
   for (int l = 0; l <= st->num_layers; ++l)
     if (!acts[l]) return rfail(RW_MISSING_ACTIVATION, "MissingActivation: no cached forward for micro-batch");
   const int L = st->num_layers;
-  // dz of the last layer: dL/dy * (1 - y^2)  (model.cpp:185-192)
+  // dz of the last layer: dL/dy * (1 - y^2)  (model.cpp:185-192) -- or
+  // already fused into the next stage's first-layer dgrad (grad_in_is_dz)
   void* cur = dz0;
   void* nxt = dz1;
-  int e = rwb::replay_dtanh_first(grad_in, acts[L], cur, uint64_t(rows) * uint64_t(st->dims[L]), stream);
-  if (e) return cfail(e, "dtanh");
+  int e = 0;
+  if (grad_in_is_dz) {
+    cur = const_cast<void*>(grad_in);
+  } else {
+    e = rwb::replay_dtanh_first(grad_in, acts[L], cur, uint64_t(rows) * uint64_t(st->dims[L]), stream);
+    if (e) return cfail(e, "dtanh");
+  }
   for (int li = L - 1; li >= 0; --li) {  // reverse layer order (model.cpp:179)
     const int64_t in = st->dims[li], out = st->dims[li + 1];
     // dW = x^T dz (:193-203), accumulated over micro-batches in order
@@ -75,6 +89,9 @@ int rw_stage_backward(const rw_stage_desc* st, int64_t rows, void* const* acts, 
       e = rwb::replay_dgrad_layer(cur, rows, in, out, st->w[li], acts[li], nxt, stream);
       if (e) return cfail(e, "dgrad GEMM");
       std::swap(cur, nxt);
+    } else if (grad_out && prev_y) {  // dz of the previous stage (same GPU), bit-identical
+      e = rwb::replay_dgrad_boundary(cur, rows, in, out, st->w[li], prev_y, grad_out, stream);
+      if (e) return cfail(e, "dgrad GEMM");
     } else if (grad_out) {
       e = rwb::replay_dgrad_layer(cur, rows, in, out, st->w[li], nullptr, grad_out, stream);
       if (e) return cfail(e, "dgrad GEMM");

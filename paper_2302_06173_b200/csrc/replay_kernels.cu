@@ -123,6 +123,17 @@ int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, co
                                                                          int(out), ep, st);
 }
 
+int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
+                          const void* y_prev_stage, void* dz_prev_stage, void* stream) {
+  gemm::EpiArgs ep{};
+  ep.out = dz_prev_stage;
+  ep.ldo = in;
+  ep.y = static_cast<const bf16*>(y_prev_stage);
+  ep.ldy = in;
+  return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BOUNDARY_DTANH_BF16>(
+      dz, out, w, out, int(rows), int(in), int(out), ep, static_cast<cudaStream_t>(stream));
+}
+
 int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
                        int accumulate, void* stream) {
   gemm::EpiArgs ep{};

@@ -39,7 +39,10 @@ enum Epi : int {
   EPI_DTANH_BF16 = 2,     // out_bf16 = acc * (1 - y[m,n]^2)           (dgrad -> next dz)
   EPI_F32 = 3,            // out_f32  = acc                             (wgrad, first mb)
   EPI_F32_ACC = 4,        // out_f32  = out_f32 + acc                   (wgrad, ordered mb sum)
+  EPI_BOUNDARY_DTANH_BF16 = 5,  // out_bf16 = bf16(acc) * (1 - y^2): a stage-boundary gradient
+                                // (rounded to bf16 as sent) fused with the previous stage's dz
 };
+__host__ __device__ constexpr bool uses_y(int epi) { return epi == EPI_DTANH_BF16 || epi == EPI_BOUNDARY_DTANH_BF16; }
 
 struct EpiArgs {
   void* out;             // bf16 or f32 [M, N] row-major, leading dim ldo (elements)
@@ -218,7 +221,7 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = tanhf(__fadd_rn(v[j], bv[j]));
-      } else if constexpr (EPI == EPI_DTANH_BF16) {
+      } else if constexpr (uses_y(EPI)) {
         const __nv_bfloat16* yp = ep.y + int64_t(row) * ep.ldy + col0;
         float yv[32];
         if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads (prefetched when yk)
@@ -238,7 +241,12 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
           for (int j = 0; j < 32; ++j) yv[j] = (col0 + j < N) ? __bfloat162float(yp[j]) : 0.f;
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) w[j] = __fmul_rn(v[j], __fsub_rn(1.f, __fmul_rn(yv[j], yv[j])));
+        for (int j = 0; j < 32; ++j) {
+          // boundary: the gradient crosses the stage boundary as bf16 (the
+          // wire value), then dtanh_first's expression, bit for bit
+          const float g = EPI == EPI_BOUNDARY_DTANH_BF16 ? __bfloat162float(__float2bfloat16_rn(v[j])) : v[j];
+          w[j] = __fmul_rn(g, __fsub_rn(1.f, __fmul_rn(yv[j], yv[j])));
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = v[j];
@@ -271,7 +279,7 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
 template <int BN, int EPI>
 __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, int n0, int M, int N, const EpiArgs& ep,
                                               const YChunk* y0 = nullptr) {
-  if constexpr (EPI == EPI_DTANH_BF16) {
+  if constexpr (uses_y(EPI)) {
     YChunk cur = *y0, nxt;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -450,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = tm * BM, n0 = tn * BN;
       const int row = m0 + ew * 32 + lane;
       YChunk y0;
-      if constexpr (EPI == EPI_DTANH_BF16) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
+      if constexpr (uses_y(EPI)) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
@@ -716,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
       const int row = tm * PM + int(rank) * BM + ew * 32 + lane;
       YChunk y0;
-      if constexpr (EPI == EPI_DTANH_BF16) load_y_chunk(ep, row, tn * BN, M, N, y0);
+      if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);

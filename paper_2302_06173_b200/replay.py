@@ -43,6 +43,10 @@ _sig = {
     "rw_stage_backward": (C.c_int, [C.POINTER(rw_stage_desc), C.c_int64, C.POINTER(C.c_void_p), C.c_void_p,
                                     C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int32,
                                     C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "rw_stage_backward_ex": (C.c_int, [C.POINTER(rw_stage_desc), C.c_int64, C.POINTER(C.c_void_p), C.c_void_p,
+                                       C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p]),
     "rw_mse_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p]),
     "rw_cast_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
@@ -162,14 +166,17 @@ class Stage:
         return acts[-1]
 
     def backward(self, acts: Sequence[torch.Tensor], grad_in: torch.Tensor, grad_out: torch.Tensor | None,
-                 accumulate: bool, dw=None, db=None, stream=None) -> None:
-        """backward_stage + ordered accumulation into self.grad (or dw/db arrays)."""
+                 accumulate: bool, dw=None, db=None, stream=None, grad_in_is_dz: bool = False,
+                 prev_y: torch.Tensor | None = None) -> None:
+        """backward_stage + ordered accumulation into self.grad (or dw/db arrays).
+        prev_y / grad_in_is_dz fuse a group-internal stage boundary (see
+        rw_stage_backward_ex): grad_out becomes the previous stage's dz."""
         rows = acts[0].shape[0]
         arr = (C.c_void_p * (self.L + 1))(*[a.data_ptr() for a in acts])
         s0, s1, sf = self._scr(rows)
-        check(LIB.rw_stage_backward(C.byref(self.desc), rows, arr, _p(grad_in), _p(grad_out),
-                                    dw or self._dw_c, db or self._db_c, int(accumulate), _p(s0), _p(s1),
-                                    _p(sf), _sh(stream)))
+        check(LIB.rw_stage_backward_ex(C.byref(self.desc), rows, arr, _p(grad_in), int(grad_in_is_dz),
+                                       _p(grad_out), _p(prev_y), dw or self._dw_c, db or self._db_c,
+                                       int(accumulate), _p(s0), _p(s1), _p(sf), _sh(stream)))
 
     def step(self, hyper: OptimizerHyper, grad: torch.Tensor | None = None, stream=None) -> None:
         """apply_layerwise_updates over this stage (reverse layer order), then
@@ -322,9 +329,13 @@ def replay_group(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, 
                 g = log.get("grad", it, mb, dev)
                 if g is None:
                     raise RwError(14, f"MissingLogData: gradient ({it}, {mb})")
+            # group-internal boundaries stay on this GPU: stage k's first-layer
+            # dgrad emits stage k-1's dz directly (bit-identical to the wire
+            # round trip + dtanh of the original run)
             for k in range(len(stages) - 1, -1, -1):
                 gout = torch.empty(rows, stages[k].dims[0], dtype=torch.bfloat16, device=dev) if k > 0 else None
-                stages[k].backward(all_acts[k], g, gout, accumulate=mb > 0)
+                stages[k].backward(all_acts[k], g, gout, accumulate=mb > 0, grad_in_is_dz=k < len(stages) - 1,
+                                   prev_y=all_acts[k - 1][-1] if k > 0 else None)
                 g = gout
         for st in reversed(stages):
             st.step(hyper)
@@ -365,7 +376,8 @@ def helper_pass(stages: Sequence[Stage], log: BoundaryLog, it: int, mbs: Sequenc
         for k in range(len(stages) - 1, -1, -1):
             gout = torch.empty(rows, stages[k].dims[0], dtype=torch.bfloat16, device=dev) if k > 0 else None
             dw, db = stages[k].grad_ptrs(bufs[k])
-            stages[k].backward(all_acts[k], g, gout, accumulate=False, dw=dw, db=db)
+            stages[k].backward(all_acts[k], g, gout, accumulate=False, dw=dw, db=db,
+                               grad_in_is_dz=k < len(stages) - 1, prev_y=all_acts[k - 1][-1] if k > 0 else None)
             g = gout
         out[mb] = bufs
     return out

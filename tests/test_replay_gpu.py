@@ -191,3 +191,41 @@ def test_training_loss_decreases():
     ghost, h = _pipeline()
     losses = [ghost.run_iteration() for _ in range(8)]
     assert all(np.isfinite(losses)) and losses[-1] < losses[0]
+
+
+def test_middle_group_fused_boundaries_bitwise():
+    """A 3-stage middle group (stages 1..3 of 5) replayed on one GPU: the two
+    group-internal boundaries use the fused dgrad -> previous-stage dz epilogue
+    (rw_stage_backward_ex); sequential replay and two parallel helpers must
+    both equal the ghost run (which exchanges bf16 gradients between stages)
+    bit for bit."""
+    h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
+    ghost = Pipeline(p=5, dim=64, hidden=96, layers=2, rows=160, micro_batches=4, seed=3, kind=ADAM, hyper=h)
+    log = BoundaryLog()
+    for it in range(3):
+        if it == 1:
+            snaps = [ghost.stages[s].snapshot() for s in (1, 2, 3)]
+        ghost.run_iteration(log_group=(1, 3), log=log)
+    mk = lambda: [Stage(s, 64, 96, 64, 2, 3, ADAM) for s in (1, 2, 3)]  # noqa: E731
+    seq = mk()
+    for st, sn in zip(seq, snaps):
+        st.restore(sn)
+    replay_group(seq, log, 1, 3, 160, 4, 3, h, first=False, last=False, dim=64)
+    helpers = [mk(), mk()]
+    for grp in helpers:
+        for st, sn in zip(grp, snaps):
+            st.restore(sn)
+    for it in range(1, 3):
+        per_mb = {}
+        for r, grp in enumerate(helpers):
+            per_mb.update(helper_pass(grp, log, it, parallel_assignment(4, 2)[r], 160, 4, 3, False, False, 64))
+        for k in range(3):
+            merged = ordered_sum([per_mb[mb][k] for mb in range(4)])
+            for grp in helpers:
+                grp[k].step(h, grad=merged)
+    for k, s in enumerate((1, 2, 3)):
+        g = ghost.stages[s].state
+        for name in ("x", "m", "v"):
+            assert torch.equal(getattr(seq[k].state, name), getattr(g, name)), (s, name)
+            for grp in helpers:
+                assert torch.equal(getattr(grp[k].state, name), getattr(g, name)), (s, name)
