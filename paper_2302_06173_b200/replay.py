@@ -348,13 +348,16 @@ def parallel_assignment(m: int, d: int) -> list[list[int]]:
 
 
 def helper_pass(stages: Sequence[Stage], log: BoundaryLog, it: int, mbs: Sequence[int], rows: int,
-                micro_batches: int, seed: int, first: bool, last: bool, dim: int) -> dict:
+                micro_batches: int, seed: int, first: bool, last: bool, dim: int, on_stage_done=None) -> dict:
     """One helper's share of iteration `it`: forward + backward of its
     micro-batches, each into its OWN flat gradient buffers (one per stage), so
-    the merge can restore the ascending-mb order exactly."""
+    the merge can restore the ascending-mb order exactly.  on_stage_done(k,
+    {mb: buffer}) fires as soon as stage k's gradients of every micro-batch of
+    this helper are complete (during the last micro-batch's backward), so the
+    merge of stage k can overlap the backward of stages k-1..0."""
     dev = stages[0].device
     out = {}
-    for mb in mbs:
+    for n_mb, mb in enumerate(mbs):
         if first:
             x = synth_inputs(seed, it, mb, rows, dim, device=dev)
         else:
@@ -373,59 +376,106 @@ def helper_pass(stages: Sequence[Stage], log: BoundaryLog, it: int, mbs: Sequenc
             if g is None:
                 raise RwError(14, f"MissingLogData: gradient ({it}, {mb})")
         bufs = [torch.empty_like(st.grad) for st in stages]
+        out[mb] = bufs
         for k in range(len(stages) - 1, -1, -1):
             gout = torch.empty(rows, stages[k].dims[0], dtype=torch.bfloat16, device=dev) if k > 0 else None
             dw, db = stages[k].grad_ptrs(bufs[k])
             stages[k].backward(all_acts[k], g, gout, accumulate=False, dw=dw, db=db,
                                grad_in_is_dz=k < len(stages) - 1, prev_y=all_acts[k - 1][-1] if k > 0 else None)
             g = gout
-        out[mb] = bufs
+            if on_stage_done is not None and n_mb == len(mbs) - 1:
+                on_stage_done(k, {b: out[b][k] for b in mbs})
     return out
+
+
+def _shard_bounds(P: int, d: int) -> tuple[int, list[tuple[int, int]]]:
+    chunk = ((P + d - 1) // d + 63) // 64 * 64
+    return chunk, [(min(P, j * chunk), min(P, (j + 1) * chunk)) for j in range(d)]
+
+
+def ordered_merge_start(bufs: dict, P: int, m: int, group=None):
+    """Start the ordered merge of one stage's gradient over the d
+    helpers: the flat gradient is sharded over the ranks; every owner sends
+    shard j of each of its micro-batches to rank j in ONE grouped batch of
+    point-to-point transfers (all links busy at once, no packing copies).
+    Asynchronous: returns a handle for ordered_merge_finish."""
+    import torch.distributed as dist
+    d, rank = dist.get_world_size(group), dist.get_rank(group)
+    glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)  # noqa: E731
+    chunk, bnd = _shard_bounds(P, d)
+    lo, hi = bnd[rank]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    recv, ops = {}, []
+    for mb in range(m):
+        owner = mb % d
+        if owner == rank:
+            for j in range(d):
+                if j != rank and bnd[j][1] > bnd[j][0]:
+                    ops.append(dist.P2POp(dist.isend, bufs[mb][bnd[j][0]:bnd[j][1]], glob(j), group))
+        elif hi > lo:
+            recv[mb] = torch.empty(hi - lo, dtype=torch.float32, device=dev)
+            ops.append(dist.P2POp(dist.irecv, recv[mb], glob(owner), group))
+    works = dist.batch_isend_irecv(ops) if ops else []
+    return dict(works=works, recv=recv, bufs=bufs, P=P, m=m, group=group, chunk=chunk, lo=lo, hi=hi, d=d, dev=dev)
+
+
+def ordered_merge_finish(h) -> torch.Tensor:
+    """Finish a merge: sum this rank's shard over micro-batches 0..m-1 in
+    ascending order (ordered_sum, bit-identical to the sequential replay) and
+    all-gather the merged shards into the full gradient."""
+    from .optim import ordered_sum
+    import torch.distributed as dist
+    for w in h["works"]:
+        w.wait()
+    lo, hi, chunk, d = h["lo"], h["hi"], h["chunk"], h["d"]
+    shard = torch.zeros(chunk, dtype=torch.float32, device=h["dev"])
+    if hi > lo:
+        parts = [h["recv"][mb] if mb in h["recv"] else h["bufs"][mb][lo:hi] for mb in range(h["m"])]
+        ordered_sum(parts, out=shard[:hi - lo])
+    full = torch.empty(chunk * d, dtype=torch.float32, device=h["dev"])
+    dist.all_gather_into_tensor(full, shard, group=h["group"])
+    return full[:h["P"]]
 
 
 def ordered_merge(per_mb: dict, k: int, m: int, group=None) -> torch.Tensor:
     """Merged gradient of stage k: ordered_sum over micro-batches 0..m-1
-    (SPEC:538).  Without a process group every micro-batch is local.  With one,
-    the flat gradient is sharded over the d ranks: each micro-batch's shard j is
-    scattered from its owner (mb mod d) to rank j, rank j sums its m shards in
-    ascending mb order, and an all-gather rebuilds the full merged gradient on
-    every rank (which then steps redundantly and identically)."""
+    (SPEC:538).  Without a process group every micro-batch is local; with one,
+    sharded point-to-point exchange + local ordered sum + all-gather (every rank
+    then steps redundantly and identically)."""
     from .optim import ordered_sum
     import torch.distributed as dist
     if group is None and not (dist.is_available() and dist.is_initialized()):
         return ordered_sum([per_mb[mb][k] for mb in range(m)])
-    d = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     any_buf = next(iter(per_mb.values()))[k]
-    P = any_buf.numel()
-    chunk = ((P + d - 1) // d + 63) // 64 * 64
-    pad = chunk * d - P
-    shards = []
-    for mb in range(m):
-        owner = mb % d
-        recv = torch.empty(chunk, dtype=torch.float32, device=any_buf.device)
-        if rank == owner:
-            src = per_mb[mb][k]
-            if pad:
-                src = torch.cat([src, src.new_zeros(pad)])
-            dist.scatter(recv, list(src.split(chunk)), src=owner, group=group)
-        else:
-            dist.scatter(recv, None, src=owner, group=group)
-        shards.append(recv)
-    merged_shard = ordered_sum(shards)
-    full = torch.empty(chunk * d, dtype=torch.float32, device=any_buf.device)
-    dist.all_gather_into_tensor(full, merged_shard, group=group)
-    return full[:P]
+    return ordered_merge_finish(ordered_merge_start({mb: b[k] for mb, b in per_mb.items()}, any_buf.numel(), m,
+                                                    group))
 
 
 def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, rows: int,
                      micro_batches: int, seed: int, hyper: OptimizerHyper, first: bool, last: bool, dim: int,
                      group=None, rank: int = 0, d: int = 1) -> int:
-    """recover_parallel for this helper rank."""
+    """recover_parallel for this helper rank.  Each stage's
+    merge starts as soon as its gradients are complete and overlaps the
+    backward of the earlier stages; the steps run after the pass."""
+    import torch.distributed as dist
     assign = parallel_assignment(micro_batches, d)
+    distributed = group is not None or (dist.is_available() and dist.is_initialized())
     for it in range(it0, it1):
-        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim)
+        handles = {}
+
+        def start(k, bufs):
+            handles[k] = ordered_merge_start(bufs, stages[k].grad.numel(), micro_batches, group)
+
+        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim,
+                             on_stage_done=start if distributed else None)
+        if distributed:
+            for k in range(len(stages) - 1, -1, -1):  # same order as the helpers that replayed
+                if k not in handles:  # this helper replayed no micro-batch
+                    start(k, {})
         for k, st in enumerate(stages):
-            merged = ordered_merge(per_mb, k, micro_batches, group)
+            if distributed:
+                merged = ordered_merge_finish(handles[k])
+            else:
+                merged = ordered_merge(per_mb, k, micro_batches, None)
             st.step(hyper, grad=merged)
     return it1 - it0

@@ -139,8 +139,23 @@ def scen_parallel_replay(rank, world):
     par = Stage(1, 64, 128, 64, 2, 11, ADAM)
     par.restore(snap)
     recover_parallel([par], log, 1, 3, 128, 4, 11, h, first=False, last=False, dim=64, rank=rank, d=world)
-    return dict(eq_seq=all(torch.equal(getattr(par.state, n), getattr(seq.state, n)) for n in ("x", "m", "v")),
-                eq_ghost=torch.equal(par.state.x, ghost.stages[1].state.x))
+    res = dict(eq_seq=all(torch.equal(getattr(par.state, n), getattr(seq.state, n)) for n in ("x", "m", "v")),
+               eq_ghost=torch.equal(par.state.x, ghost.stages[1].state.x))
+    # a 3-stage middle group, odd micro-batch count (uneven helpers), merges
+    # overlapped with the backward of the earlier stages
+    g5 = Pipeline(p=5, dim=64, hidden=96, layers=2, rows=96, micro_batches=5, seed=4, kind=ADAM, hyper=h)
+    log5 = BoundaryLog()
+    for it in range(3):
+        if it == 1:
+            snaps = [g5.stages[s].snapshot() for s in (1, 2, 3)]
+        g5.run_iteration(log_group=(1, 3), log=log5)
+    grp = [Stage(s, 64, 96, 64, 2, 4, ADAM) for s in (1, 2, 3)]
+    for st, sn in zip(grp, snaps):
+        st.restore(sn)
+    recover_parallel(grp, log5, 1, 3, 96, 5, 4, h, first=False, last=False, dim=64, rank=rank, d=world)
+    res["eq_group"] = all(torch.equal(getattr(grp[k].state, n), getattr(g5.stages[s].state, n))
+                          for k, s in enumerate((1, 2, 3)) for n in ("x", "m", "v"))
+    return res
 
 
 @needs2
@@ -148,3 +163,4 @@ def test_parallel_replay_two_ranks_bitexact():
     out = _run(scen_parallel_replay)
     for r in (0, 1):
         assert out[r]["eq_seq"] and out[r]["eq_ghost"]
+        assert out[r]["eq_group"]
