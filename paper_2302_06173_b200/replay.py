@@ -454,9 +454,10 @@ def ordered_merge(per_mb: dict, k: int, m: int, group=None) -> torch.Tensor:
 def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, rows: int,
                      micro_batches: int, seed: int, hyper: OptimizerHyper, first: bool, last: bool, dim: int,
                      group=None, rank: int = 0, d: int = 1) -> int:
-    """recover_parallel for this helper rank.  Each stage's
-    merge starts as soon as its gradients are complete and overlaps the
-    backward of the earlier stages; the steps run after the pass."""
+    """recover_parallel for this helper rank: replay this
+    helper's micro-batches, then all stages' merges in flight together
+    (grouped point-to-point shard exchange), then the ordered sums, the
+    all-gathers and the steps."""
     import torch.distributed as dist
     assign = parallel_assignment(micro_batches, d)
     distributed = group is not None or (dist.is_available() and dist.is_initialized())
@@ -466,12 +467,13 @@ def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: i
         def start(k, bufs):
             handles[k] = ordered_merge_start(bufs, stages[k].grad.numel(), micro_batches, group)
 
-        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim,
-                             on_stage_done=start if distributed else None)
+        # Merges are NOT overlapped with the backward: NCCL's kernels would
+        # take SMs from the persistent GEMM grid, whose static tile schedule
+        # then waits for its last CTA (measured 1.7x slower at N=4).
+        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim)
         if distributed:
-            for k in range(len(stages) - 1, -1, -1):  # same order as the helpers that replayed
-                if k not in handles:  # this helper replayed no micro-batch
-                    start(k, {})
+            for k in range(len(stages) - 1, -1, -1):
+                start(k, {mb: per_mb[mb][k] for mb in assign[rank]})
         for k, st in enumerate(stages):
             if distributed:
                 merged = ordered_merge_finish(handles[k])
