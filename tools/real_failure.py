@@ -30,8 +30,13 @@ def _sizes(which):
 
 
 def _crcs(st):
+    """CRC32 of each buffer's group contents (inter-group padding excluded)."""
     from paper_2302_06173_b200.logstore import crc32_device
-    return [crc32_device(getattr(st, n).view(torch.uint8)) for n in ("x", "m", "v")]
+    out = []
+    for n in ("x", "m", "v"):
+        packed = torch.cat([st.view(n, i) for i in range(st.num_groups)])
+        out.append(crc32_device(packed.view(torch.uint8)))
+    return out
 
 
 def member(rank, port, which, q):
@@ -63,14 +68,16 @@ def member(rank, port, which, q):
     plan = mem.publish_plan(settle=0.05)
     mem.stop()
     join_generation(store, plan, rank, "nccl", device_id=torch.device("cuda", rank))
-    t_join = time.time()
+    dist.all_reduce(torch.zeros(1, device="cuda"))  # connect the new communicator
     torch.cuda.synchronize()
+    t_join = time.time()
     p = resolve(st.markers(), h, lens=sizes)
     used, nbytes = recover(st, h, p, src=0)
     torch.cuda.synchronize()
     t_rec = time.time()
     crash = float(store.get("crash_time"))
-    q.put(("survivor", dict(detect_ms=(mem.detected_at - crash) * 1e3, repair_ms=(t_join - t_det) * 1e3,
+    q.put(("survivor", dict(detect_ms=(mem.detected_at - crash) * 1e3,
+                            repair_ms=(t_join - t_det) * 1e3,  # abort + plan + replacement joins + connect
                             recovery_ms=(t_rec - t_join) * 1e3, total_ms=(t_rec - crash) * 1e3,
                             strategy=p.strategy, undo_groups=len(p.undo_ids), transfer=used, bytes=nbytes,
                             crcs=_crcs(st), markers=st.markers()[:3])))
@@ -84,11 +91,15 @@ def replacement(port, which, q):
     import datetime
     store = dist.TCPStore("127.0.0.1", port, is_master=False, timeout=datetime.timedelta(seconds=120))
     sizes = _sizes(which)
+    # hot spare: the replica buffers are allocated on the spare GPU before any
+    # failure (the spare of a real job has its own GPU; here it is the one the
+    # crashed rank frees, so the allocation waits for the slot)
     plan, rank = claim_slot(store, 0, timeout=120)
     torch.cuda.set_device(rank)
-    st = DeviceState(sizes, kind=ADAM)            # empty replica on the freed GPU
+    st = DeviceState(sizes, kind=ADAM)
     h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
     join_generation(store, plan, rank, "nccl", device_id=torch.device("cuda", rank))
+    dist.all_reduce(torch.zeros(1, device="cuda"))
     p = resolve([], h)
     used, nbytes = recover(st, h, p, src=0)
     torch.cuda.synchronize()
