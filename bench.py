@@ -388,7 +388,8 @@ def checkpoint_bench(sizes, reps: int = 2) -> dict:
         w, l_ = min(wt), min(lt)
         return dict(bytes=nbytes, dir=root, write_s=round(w, 3), write_gbs=round(nbytes / w / 1e9, 2),
                     load_s=round(l_, 3), load_gbs=round(nbytes / l_ / 1e9, 2), bit_exact=bool(ok),
-                    path="native pinned ring (3 x 64 MiB), GPU CRC32, fsync + atomic manifest")
+                    path="native: 8 I/O workers x (32 MiB pinned chunk + copy stream), one part file each, "
+                         "GPU CRC32, fsync + atomic manifest")
     finally:
         shutil.rmtree(d, ignore_errors=True)
         del st

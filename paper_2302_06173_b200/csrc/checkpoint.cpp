@@ -6,7 +6,8 @@
 // gives its atomic-write idiom (write .tmp, rename), which is kept here.
 //
 // On-disk layout under `dir`:
-//   ck_<iter:016>/w<worker:05>/<blob>.bin   raw bytes of one buffer
+//   ck_<iter:016>/w<worker:05>/<blob>.bin   raw bytes of a host buffer, or
+//   ck_<iter:016>/w<worker:05>/<blob>.bin.<k>  part k of a device buffer
 //   ck_<iter:016>/w<worker:05>.wm           worker manifest: names, sizes, CRC32s
 //   MANIFEST_<iter:016>                     global commit marker
 // Commit order: blobs written + fsync'd -> worker manifest (tmp, fsync,
@@ -14,9 +15,10 @@
 // Hence "manifest visible <=> all blobs fully written"; a crash anywhere
 // before the final rename leaves the previous MANIFEST the latest valid one.
 //
-// Data path: device buffers move through a ring of pinned chunks; the D2H
-// copy of chunk c+1, c+2 overlaps the write(2) of chunk c (and H2D overlaps
-// pread on load).  Each device blob's CRC32 (the wire.cpp polynomial) is
+// Data path: device buffers move in 32 MiB chunks through 8 I/O workers,
+// each with its own pinned chunk and copy stream (D2H + pwrite / pread +
+// H2D at the chunk's file offset), so PCIe copies, page-cache copies and the
+// storage work in parallel.  Each device blob's CRC32 (the wire.cpp polynomial) is
 // computed on the GPU at HBM speed; load recomputes it on the GPU after the
 // H2D and compares with the manifest.
 #include <cuda_runtime.h>
@@ -34,6 +36,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -51,8 +54,8 @@ int cfail(int code, const std::string& msg) {
                                                            cudaGetErrorString(e_));              \
   } while (0)
 
-constexpr uint64_t kChunk = 64ull << 20;  // pinned staging chunk
-constexpr int kRing = 3;
+constexpr uint64_t kChunk = 32ull << 20;  // pinned staging chunk per worker
+constexpr int kWorkers = 8;                // I/O threads, each with its own stream + buffer
 
 // CRC32 (reflected 0xEDB88320), the wire.cpp:31-38 function, for host blobs
 uint32_t crc32_host(const void* p, uint64_t n) {
@@ -72,11 +75,13 @@ uint32_t crc32_host(const void* p, uint64_t n) {
   return c ^ 0xFFFFFFFFu;
 }
 
-// one pinned ring shared by all calls (allocation of pinned memory is slow)
+// Staging pool shared by all calls (allocating pinned memory is slow): one
+// pinned chunk + one copy stream per I/O worker.
 struct Ring {
   std::mutex mu;
-  void* buf[kRing] = {};
-  cudaEvent_t ev[kRing] = {};
+  void* buf[kWorkers] = {};
+  cudaStream_t st[kWorkers] = {};
+  cudaEvent_t start = nullptr;
   uint32_t* d_crc = nullptr;
   uint32_t* d_scratch = nullptr;
   uint64_t scratch_words = 0;
@@ -89,23 +94,123 @@ int ring_ready(Ring& R) {
   CCUDA(cudaGetDevice(&dev));
   if (R.device == dev && R.buf[0]) return RW_OK;
   if (R.buf[0]) {  // different device: rebuild on this one
-    for (int i = 0; i < kRing; ++i) {
+    for (int i = 0; i < kWorkers; ++i) {
       cudaFreeHost(R.buf[i]);
-      cudaEventDestroy(R.ev[i]);
+      cudaStreamDestroy(R.st[i]);
       R.buf[i] = nullptr;
     }
+    cudaEventDestroy(R.start);
     cudaFree(R.d_crc);
     cudaFree(R.d_scratch);
     R.d_crc = nullptr;
     R.d_scratch = nullptr;
     R.scratch_words = 0;
   }
-  for (int i = 0; i < kRing; ++i) {
+  for (int i = 0; i < kWorkers; ++i) {
     CCUDA(cudaMallocHost(&R.buf[i], kChunk));
-    CCUDA(cudaEventCreateWithFlags(&R.ev[i], cudaEventDisableTiming));
+    CCUDA(cudaStreamCreateWithFlags(&R.st[i], cudaStreamNonBlocking));
   }
+  CCUDA(cudaEventCreateWithFlags(&R.start, cudaEventDisableTiming));
   CCUDA(cudaMalloc(&R.d_crc, sizeof(uint32_t)));
   R.device = dev;
+  return RW_OK;
+}
+
+// Move one device blob to (to_file) or from its part files: the blob's
+// kChunk pieces are split into nparts contiguous parts, worker w moves part w
+// (one async copy on its own stream + one pwrite/pread per chunk) into its own
+// file, so the copies, the page cache and the storage run in parallel and no
+// two writers share an inode lock.  Ordered after prior work on `cs`;
+// complete (host-synchronised) on return.
+uint32_t parts_for(uint64_t bytes) {
+  const uint64_t nch = (bytes + kChunk - 1) / kChunk;
+  return static_cast<uint32_t>(std::max<uint64_t>(1, std::min<uint64_t>(kWorkers, nch)));
+}
+uint64_t part_chunks(uint64_t bytes, uint32_t nparts) {
+  const uint64_t nch = (bytes + kChunk - 1) / kChunk;
+  return (nch + nparts - 1) / nparts;
+}
+uint64_t part_bytes(uint64_t bytes, uint32_t nparts, uint32_t w) {
+  const uint64_t per = part_chunks(bytes, nparts) * kChunk;
+  const uint64_t lo = std::min<uint64_t>(bytes, w * per), hi = std::min<uint64_t>(bytes, (w + 1) * per);
+  return hi - lo;
+}
+std::string part_path(const std::string& base, uint32_t w) { return base + "." + std::to_string(w); }
+
+int staged_io(Ring& R, bool to_file, const std::vector<int>& fds, void* dev, uint64_t bytes, cudaStream_t cs,
+              const std::string& path) {
+  int device = 0;
+  CCUDA(cudaGetDevice(&device));
+  CCUDA(cudaEventRecord(R.start, cs));
+  const uint32_t nparts = static_cast<uint32_t>(fds.size());
+  const uint64_t nch = (bytes + kChunk - 1) / kChunk, per = part_chunks(bytes, nparts);
+  std::vector<int> status(nparts, RW_OK);
+  std::vector<std::string> errs(nparts);
+  auto work = [&](uint32_t w) {
+    if (cudaSetDevice(device) != cudaSuccess || cudaStreamWaitEvent(R.st[w], R.start, 0) != cudaSuccess) {
+      status[w] = RW_CUDA_ERROR;
+      errs[w] = "checkpoint worker setup failed";
+      return;
+    }
+    const int fd = fds[w];
+    for (uint64_t c = w * per; c < std::min<uint64_t>(nch, (w + 1) * per); ++c) {
+      const uint64_t off = c * kChunk, len = std::min(kChunk, bytes - off), foff = off - w * per * kChunk;
+      char* d = static_cast<char*>(dev) + off;
+      if (to_file) {
+        if (cudaMemcpyAsync(R.buf[w], d, len, cudaMemcpyDeviceToHost, R.st[w]) != cudaSuccess ||
+            cudaStreamSynchronize(R.st[w]) != cudaSuccess) {
+          status[w] = RW_CUDA_ERROR;
+          errs[w] = "checkpoint D2H failed";
+          return;
+        }
+        const char* p = static_cast<const char*>(R.buf[w]);
+        uint64_t left = len, at = foff;
+        while (left) {
+          const ssize_t k = ::pwrite(fd, p, left, static_cast<off_t>(at));
+          if (k < 0 && errno == EINTR) continue;
+          if (k <= 0) {
+            status[w] = RW_STORAGE_ERROR;
+            errs[w] = "StorageError: short write on " + part_path(path, w);
+            return;
+          }
+          p += k;
+          at += uint64_t(k);
+          left -= uint64_t(k);
+        }
+      } else {
+        char* p = static_cast<char*>(R.buf[w]);
+        uint64_t left = len, at = foff;
+        while (left) {
+          const ssize_t k = ::pread(fd, p, left, static_cast<off_t>(at));
+          if (k < 0 && errno == EINTR) continue;
+          if (k <= 0) {
+            status[w] = RW_STORAGE_ERROR;
+            errs[w] = "StorageError: short read on " + part_path(path, w);
+            return;
+          }
+          p += k;
+          at += uint64_t(k);
+          left -= uint64_t(k);
+        }
+        if (cudaMemcpyAsync(d, R.buf[w], len, cudaMemcpyHostToDevice, R.st[w]) != cudaSuccess ||
+            cudaStreamSynchronize(R.st[w]) != cudaSuccess) {
+          status[w] = RW_CUDA_ERROR;
+          errs[w] = "checkpoint H2D failed";
+          return;
+        }
+      }
+    }
+    if (to_file && ::fsync(fd) != 0) {
+      status[w] = RW_STORAGE_ERROR;
+      errs[w] = "StorageError: fsync failed on " + part_path(path, w);
+    }
+  };
+  std::vector<std::thread> th;
+  for (uint32_t w = 1; w < nparts; ++w) th.emplace_back(work, w);
+  work(0);
+  for (auto& t : th) t.join();
+  for (uint32_t w = 0; w < nparts; ++w)
+    if (status[w]) return cfail(status[w], errs[w]);
   return RW_OK;
 }
 
@@ -223,6 +328,7 @@ bool read_text(const std::string& path, std::string* out) {
 struct BlobEntry {
   uint64_t bytes = 0;
   uint32_t crc = 0;
+  uint32_t parts = 0;  // 0: one file <name>.bin; else <name>.bin.<k>, k < parts
 };
 
 // worker manifest: "SWCK 1\niteration I\nworker W\nblob <name> <bytes> <crc hex>\n...end\n"
@@ -248,7 +354,12 @@ bool parse_worker_manifest(const std::string& text, uint64_t it, uint32_t w, std
       if (b != w) return false;
       saw_w = true;
     } else if (std::sscanf(line.c_str(), "blob %255s %llu %x", name, &a, &crc) == 3) {
-      (*out)[name] = BlobEntry{a, crc};
+      unsigned parts = 0;
+      char n2[256];
+      unsigned long long a2 = 0;
+      unsigned c2 = 0;
+      if (std::sscanf(line.c_str(), "blob %255s %llu %x %u", n2, &a2, &c2, &parts) != 4) parts = 0;
+      (*out)[name] = BlobEntry{a, crc, parts};
     } else if (line == "end") {
       ended = true;
       break;
@@ -298,40 +409,30 @@ int rw_ckpt_write(const char* dir, uint64_t iteration, uint32_t worker, const rw
       return cfail(RW_STORAGE_ERROR, "StorageError: injected crash during checkpoint write");
     const rw_blob& b = blobs[i];
     const std::string path = wdir + "/" + b.name + ".bin";
-    int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
-    if (fd < 0) return cfail(RW_STORAGE_ERROR, "StorageError: cannot open " + path);
-    uint32_t crc = 0;
-    if (b.on_host) {
+    uint32_t crc = 0, nparts = 0;
+    if (b.on_host || b.bytes == 0) {
+      int fd = ::open(path.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+      if (fd < 0) return cfail(RW_STORAGE_ERROR, "StorageError: cannot open " + path);
       crc = crc32_host(b.data, b.bytes);
       st = write_all(fd, b.data, b.bytes, path);
-    } else if (b.bytes) {
-      st = device_crc(g_ring, b.data, b.bytes, cs, &crc);
-      const uint64_t nch = (b.bytes + kChunk - 1) / kChunk;
-      auto issue = [&](uint64_t c) -> int {
-        const uint64_t off = c * kChunk, len = std::min(kChunk, b.bytes - off);
-        CCUDA(cudaMemcpyAsync(g_ring.buf[c % kRing], static_cast<const char*>(b.data) + off, len,
-                              cudaMemcpyDeviceToHost, cs));
-        CCUDA(cudaEventRecord(g_ring.ev[c % kRing], cs));
-        return RW_OK;
-      };
-      for (uint64_t c = 0; !st && c < std::min<uint64_t>(nch, kRing - 1); ++c) st = issue(c);
-      for (uint64_t c = 0; !st && c < nch; ++c) {
-        if (c + kRing - 1 < nch) st = issue(c + kRing - 1);  // its buffer's previous write is done
-        if (st) break;
-        if (cudaEventSynchronize(g_ring.ev[c % kRing]) != cudaSuccess) {
-          st = cfail(RW_CUDA_ERROR, "checkpoint D2H failed");
-          break;
-        }
-        const uint64_t off = c * kChunk, len = std::min(kChunk, b.bytes - off);
-        st = write_all(fd, g_ring.buf[c % kRing], len, path);
+      if (!st && ::fsync(fd) != 0) st = cfail(RW_STORAGE_ERROR, "StorageError: fsync failed on " + path);
+      ::close(fd);
+    } else {
+      nparts = parts_for(b.bytes);
+      std::vector<int> fds;
+      for (uint32_t w = 0; w < nparts && !st; ++w) {
+        const int fd = ::open(part_path(path, w).c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+        if (fd < 0) st = cfail(RW_STORAGE_ERROR, "StorageError: cannot open " + part_path(path, w));
+        else fds.push_back(fd);
       }
-      if (st) cudaStreamSynchronize(cs);
+      if (!st) st = device_crc(g_ring, b.data, b.bytes, cs, &crc);
+      if (!st) st = staged_io(g_ring, true, fds, b.data, b.bytes, cs, path);
+      for (int fd : fds) ::close(fd);
     }
-    if (!st && ::fsync(fd) != 0) st = cfail(RW_STORAGE_ERROR, "StorageError: fsync failed on " + path);
-    ::close(fd);
     if (st) return st;
     char line[320];
-    std::snprintf(line, sizeof(line), "blob %s %llu %08x\n", b.name, static_cast<unsigned long long>(b.bytes), crc);
+    std::snprintf(line, sizeof(line), "blob %s %llu %08x %u\n", b.name, static_cast<unsigned long long>(b.bytes),
+                  crc, nparts);
     wm += line;
   }
   wm += "end\n";
@@ -430,41 +531,44 @@ int rw_ckpt_load(const char* dir, uint64_t iteration, uint32_t worker, const rw_
     const rw_blob& b = blobs[i];
     const BlobEntry& ent = m[b.name];
     const std::string path = wdir + "/" + b.name + ".bin";
-    int fd = ::open(path.c_str(), O_RDONLY);
-    if (fd < 0) return cfail(RW_STORAGE_ERROR, "StorageError: cannot open " + path);
-    struct stat sb;
-    if (::fstat(fd, &sb) != 0 || static_cast<uint64_t>(sb.st_size) != ent.bytes) {
-      ::close(fd);
-      return cfail(RW_STORAGE_ERROR, "StorageError: truncated blob " + path);
+    const uint32_t nfiles = ent.parts ? ent.parts : 1;
+    std::vector<int> fds;
+    for (uint32_t w = 0; w < nfiles && !st; ++w) {
+      const std::string fp = ent.parts ? part_path(path, w) : path;
+      const uint64_t want = ent.parts ? part_bytes(ent.bytes, ent.parts, w) : ent.bytes;
+      const int fd = ::open(fp.c_str(), O_RDONLY);
+      struct stat sb;
+      if (fd < 0) {
+        st = cfail(RW_STORAGE_ERROR, "StorageError: cannot open " + fp);
+      } else {
+        fds.push_back(fd);
+        if (::fstat(fd, &sb) != 0 || static_cast<uint64_t>(sb.st_size) != want)
+          st = cfail(RW_STORAGE_ERROR, "StorageError: truncated blob " + fp);
+      }
     }
     uint32_t crc = 0;
-    if (b.on_host) {
-      st = read_all(fd, b.data, b.bytes, 0, path);
-      if (!st) crc = crc32_host(b.data, b.bytes);
-    } else if (b.bytes) {
-      const uint64_t nch = (b.bytes + kChunk - 1) / kChunk;
-      bool pending[kRing] = {};
-      for (uint64_t c = 0; !st && c < nch; ++c) {
-        const int k = static_cast<int>(c % kRing);
-        if (pending[k] && cudaEventSynchronize(g_ring.ev[k]) != cudaSuccess) {
-          st = cfail(RW_CUDA_ERROR, "checkpoint H2D failed");
-          break;
-        }
-        const uint64_t off = c * kChunk, len = std::min(kChunk, b.bytes - off);
-        st = read_all(fd, g_ring.buf[k], len, off, path);
-        if (st) break;
-        if (cudaMemcpyAsync(static_cast<char*>(b.data) + off, g_ring.buf[k], len, cudaMemcpyHostToDevice, cs) !=
-                cudaSuccess ||
-            cudaEventRecord(g_ring.ev[k], cs) != cudaSuccess) {
-          st = cfail(RW_CUDA_ERROR, "checkpoint H2D failed");
-          break;
-        }
-        pending[k] = true;
+    if (st) {
+    } else if (!ent.parts) {  // single file: host blob or a device blob written as one
+      if (b.on_host) {
+        st = read_all(fds[0], b.data, b.bytes, 0, path);
+        if (!st) crc = crc32_host(b.data, b.bytes);
+      } else if (b.bytes) {
+        st = staged_io(g_ring, false, fds, b.data, b.bytes, cs, path);
+        if (!st) st = device_crc(g_ring, b.data, b.bytes, cs, &crc);
       }
+    } else if (b.on_host) {  // device-written parts into a host buffer
+      uint64_t off = 0;
+      for (uint32_t w = 0; w < ent.parts && !st; ++w) {
+        const uint64_t pb = part_bytes(ent.bytes, ent.parts, w);
+        st = read_all(fds[w], static_cast<char*>(b.data) + off, pb, 0, part_path(path, w));
+        off += pb;
+      }
+      if (!st) crc = crc32_host(b.data, b.bytes);
+    } else {
+      st = staged_io(g_ring, false, fds, b.data, b.bytes, cs, path);
       if (!st) st = device_crc(g_ring, b.data, b.bytes, cs, &crc);
-      else cudaStreamSynchronize(cs);
     }
-    ::close(fd);
+    for (int fd : fds) ::close(fd);
     if (st) return st;
     if (crc != ent.crc) return cfail(RW_STORAGE_ERROR, "StorageError: checksum mismatch in " + path);
   }

@@ -52,11 +52,12 @@ def test_device_roundtrip_bitexact(tmp_path):
         load_checkpoint([DeviceState([5, 5], kind=ADAM), rb], str(tmp_path))
     assert e.value.name == "ShapeMismatch"
     # device-side CRC catches a flipped byte deep inside a multi-chunk blob
-    p = tmp_path / "ck_0000000000000040" / "w00000" / "s0.m.bin"
-    with open(p, "r+b") as f:
-        f.seek(70 << 20)
+    parts = sorted((tmp_path / "ck_0000000000000040" / "w00000").glob("s0.m.bin.*"))
+    assert len(parts) == 3  # 96 MB blob -> three 32 MiB parts written in parallel
+    with open(parts[-1], "r+b") as f:
+        f.seek(6 << 20)
         c = f.read(1)
-        f.seek(70 << 20)
+        f.seek(6 << 20)
         f.write(bytes([c[0] ^ 1]))
     with pytest.raises(RwError) as e:
         load_checkpoint([ra, rb], str(tmp_path))
