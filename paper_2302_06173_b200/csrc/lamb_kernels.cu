@@ -53,24 +53,31 @@ struct V16<double> {
   static constexpr int n = 2;
 };
 
+// m, v advance and the two squared-norm contributions of one element
 template <typename T>
-__device__ __forceinline__ void lamb_elem(const T* __restrict__ x, T* __restrict__ g, const T* __restrict__ grad,
-                                          T* __restrict__ m, T* __restrict__ v, uint64_t k, const T c1, const T c2,
+__device__ __forceinline__ void lamb_math(const T xk, const T gd, T& mk, T& vk, const T c1, const T c2,
                                           const Uniform& u, double& sx, double& su) {
   using A = LA<T>;
-  const T gd = grad ? grad[k] : g[k];
-  if (grad) g[k] = gd;  // block.g = grad (optim.cpp:349)
-  const T mk = A::add(A::mul(T(u.b1), m[k]), A::mul(T(u.one_m_b1), gd));
-  const T vk = A::add(A::mul(T(u.b2), v[k]), A::mul(A::mul(T(u.one_m_b2), gd), gd));
-  m[k] = mk;
-  v[k] = vk;
+  mk = A::add(A::mul(T(u.b1), mk), A::mul(T(u.one_m_b1), gd));
+  vk = A::add(A::mul(T(u.b2), vk), A::mul(A::mul(T(u.one_m_b2), gd), gd));
   const T mhat = A::div(mk, c1);
   const T vhat = A::div(vk, c2);
-  const T xk = x[k];
   const T upd = A::add(A::div(mhat, A::add(A::sqrt(vhat), T(u.eps))), A::mul(T(u.wd), xk));
   const double xd = double(xk), ud = double(upd);
   sx = __dadd_rn(sx, __dmul_rn(xd, xd));
   su = __dadd_rn(su, __dmul_rn(ud, ud));
+}
+
+template <typename T>
+__device__ __forceinline__ void lamb_elem(const T* __restrict__ x, T* __restrict__ g, const T* __restrict__ grad,
+                                          T* __restrict__ m, T* __restrict__ v, uint64_t k, const T c1, const T c2,
+                                          const Uniform& u, double& sx, double& su) {
+  const T gd = grad ? grad[k] : g[k];
+  if (grad) g[k] = gd;  // block.g = grad (optim.cpp:349)
+  T mk = m[k], vk = v[k];
+  lamb_math<T>(x[k], gd, mk, vk, c1, c2, u, sx, su);
+  m[k] = mk;
+  v[k] = vk;
 }
 
 // Pass 1 over ALL selected groups in one launch: one warp per chunk (the same
@@ -99,7 +106,30 @@ __global__ void __launch_bounds__(kLT) lamb_pass1_kernel(const T* __restrict__ x
     const uint64_t begin = w.off + uint64_t(c - w.chunk_begin) * chunk_elems;
     const uint64_t end = min(begin + chunk_elems, w.off + w.len);
     double sx = 0.0, su = 0.0;
-    for (uint64_t k = begin + lane; k < end; k += 32) lamb_elem<T>(x, g, grad, m, v, k, c1, c2, u, sx, su);
+    // unaligned head, 16-byte vector body (4 fp32 / 2 fp64 per lane), tail
+    constexpr int EV = V16<T>::n;
+    using VT = typename V16<T>::type;
+    uint64_t a16 = (begin + EV - 1) / EV * EV;
+    if (a16 > end) a16 = end;
+    const uint64_t b16 = a16 + (end - a16) / EV * EV;
+    for (uint64_t k = begin + lane; k < a16; k += 32) lamb_elem<T>(x, g, grad, m, v, k, c1, c2, u, sx, su);
+#pragma unroll 4
+    for (uint64_t k = a16 + uint64_t(lane) * EV; k < b16; k += 32 * EV) {
+      const VT xv = *reinterpret_cast<const VT*>(x + k);
+      VT gv = *reinterpret_cast<const VT*>((grad ? grad : g) + k);
+      VT mv = *reinterpret_cast<const VT*>(m + k);
+      VT vv = *reinterpret_cast<const VT*>(v + k);
+      const T* xp = reinterpret_cast<const T*>(&xv);
+      const T* gp = reinterpret_cast<const T*>(&gv);
+      T* mp = reinterpret_cast<T*>(&mv);
+      T* vp = reinterpret_cast<T*>(&vv);
+#pragma unroll
+      for (int e = 0; e < EV; ++e) lamb_math<T>(xp[e], gp[e], mp[e], vp[e], c1, c2, u, sx, su);
+      *reinterpret_cast<VT*>(m + k) = mv;
+      *reinterpret_cast<VT*>(v + k) = vv;
+      if (grad) *reinterpret_cast<VT*>(g + k) = gv;  // block.g = grad (optim.cpp:349)
+    }
+    for (uint64_t k = b16 + lane; k < end; k += 32) lamb_elem<T>(x, g, grad, m, v, k, c1, c2, u, sx, su);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       sx = __dadd_rn(sx, __shfl_xor_sync(0xffffffffu, sx, o));

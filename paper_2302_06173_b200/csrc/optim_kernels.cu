@@ -170,6 +170,10 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
 
 template <int KIND>
 struct Uses {
+  // g is read by every pass except LAMB's step x-pass (its gradient was
+  // consumed by the norm pass)
+  template <bool UNDO>
+  static constexpr bool g = !(KIND == RW_LAMB && !UNDO);
   static constexpr bool m = KIND != RW_SGD;
   static constexpr bool v = KIND == RW_ADAM || KIND == RW_ADAMW || KIND == RW_AMSGRAD || KIND == RW_LAMB;
   static constexpr bool vmax = KIND == RW_AMSGRAD;
@@ -342,11 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     mt.copy = (PUSH && (cur_flags & kWorkCopyOnly)) ? 1u : 0u;
     mt.ss = cur_ss;
     const uint32_t bytes = mt.nbulk * sizeof(T);
-    constexpr int nload = 2 + (U::m ? 1 : 0) + (U::v ? 1 : 0) + (U::vmax ? 1 : 0);
+    constexpr bool kG = U::template g<UNDO> || PUSH;
+    constexpr int nload = 1 + (kG ? 1 : 0) + (U::m ? 1 : 0) + (U::v ? 1 : 0) + (U::vmax ? 1 : 0);
     mbar_expect_tx(&full[st], bytes * nload);
     if (bytes) {
       bulk_load(slot(st, SX), x + a16, bytes, &full[st]);
-      bulk_load(slot(st, SG), gsrc + a16, bytes, &full[st]);
+      if constexpr (kG) bulk_load(slot(st, SG), gsrc + a16, bytes, &full[st]);
       if constexpr (U::m) bulk_load(slot(st, SM), m + a16, bytes, &full[st]);
       if constexpr (U::v) bulk_load(slot(st, SV), v + a16, bytes, &full[st]);
       if constexpr (U::vmax) bulk_load(slot(st, SW), vmax + a16, bytes, &full[st]);
@@ -410,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
     T zero_m = T(0), zero_v = T(0), zero_w = T(0);
     auto body = [&](uint32_t e) {
       V xr = *reinterpret_cast<const V*>(xs + e);
-      V gr = *reinterpret_cast<const V*>(gs + e);
+      V gr{};
+      if constexpr (U::template g<UNDO> || PUSH) gr = *reinterpret_cast<const V*>(gs + e);
       V mr, vr, wr;
       if constexpr (U::m) mr = *reinterpret_cast<const V*>(ms + e);
       if constexpr (U::v) vr = *reinterpret_cast<const V*>(vs + e);
