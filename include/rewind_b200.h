@@ -301,6 +301,12 @@ int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* act
                          float* const* db, int32_t accumulate, void* scratch_dz0, void* scratch_dz1,
                          float* scratch_f32, void* stream);
 
+/* Keep n SMs free of the replay GEMM grids (0 = use every SM), so that
+ * collectives issued concurrently (parallel-recovery merges) get SMs: the
+ * persistent GEMM's static tile schedule would otherwise wait for its last
+ * CTA behind a collective kernel.  Process-wide. */
+int rw_replay_set_sm_reserve(int32_t n);
+
 /* mse_loss (model.cpp:174-188): grad = 2/(n*micro_batches) * (pred - target)
  * (bf16 out); *loss (device double, may be NULL) = mean squared error.
  * scratch: 256 doubles. */

@@ -109,6 +109,8 @@ int rw_mse_grad(const void* pred, const float* target, uint64_t n, uint64_t micr
   return RW_OK;
 }
 
+int rw_replay_set_sm_reserve(int32_t n) { return rwb::replay_set_sm_reserve(n); }
+
 int rw_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream) {
   if (!in || !out) return rfail(RW_INVALID_ARGUMENT, "null argument");
   int e = rwb::replay_cast_bf16(in, out, n, stream);

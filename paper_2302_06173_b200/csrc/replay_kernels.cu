@@ -96,6 +96,25 @@ int grid1d(uint64_t n) {
 
 }  // namespace
 
+// SMs kept free of the GEMM grid while collectives run concurrently (a
+// persistent grid with a static tile schedule waits for its last CTA, so a
+// collective kernel holding one SM would stall the whole GEMM).
+static int g_sm_reserve = 0;
+int replay_set_sm_reserve(int n) {
+  g_sm_reserve = n < 0 ? 0 : n;
+  return 0;
+}
+static int gemm_cap() {
+  if (g_sm_reserve == 0) return 0;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms - g_sm_reserve > 1 ? sms - g_sm_reserve : 1;
+}
+
 int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, const void* w, const float* b,
                          void* y, void* stream) {
   gemm::EpiArgs ep{};
@@ -104,7 +123,7 @@ int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, c
   ep.bias = b;
   // Y[R,out] = X[R,in] . W[in,out]: A = X (K-major), B = W viewed [out,in] (MN-major)
   return gemm::launch<kBN, gemm::K_MAJOR, gemm::MN_MAJOR, gemm::EPI_BIAS_TANH_BF16>(
-      x, in, w, out, int(rows), int(out), int(in), ep, static_cast<cudaStream_t>(stream));
+      x, in, w, out, int(rows), int(out), int(in), ep, static_cast<cudaStream_t>(stream), gemm_cap());
 }
 
 int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
@@ -118,9 +137,9 @@ int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, co
   // dX[R,in] = dZ[R,out] . W[in,out]^T: A = dZ (K-major), B = W as [in,out] (K-major)
   if (y_prev)
     return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_DTANH_BF16>(dz, out, w, out, int(rows),
-                                                                                 int(in), int(out), ep, st);
+                                                                                 int(in), int(out), ep, st, gemm_cap());
   return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BF16>(dz, out, w, out, int(rows), int(in),
-                                                                         int(out), ep, st);
+                                                                         int(out), ep, st, gemm_cap());
 }
 
 int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
@@ -131,7 +150,7 @@ int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out,
   ep.y = static_cast<const bf16*>(y_prev_stage);
   ep.ldy = in;
   return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BOUNDARY_DTANH_BF16>(
-      dz, out, w, out, int(rows), int(in), int(out), ep, static_cast<cudaStream_t>(stream));
+      dz, out, w, out, int(rows), int(in), int(out), ep, static_cast<cudaStream_t>(stream), gemm_cap());
 }
 
 int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
@@ -143,9 +162,9 @@ int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, 
   // dW[in,out] = X[R,in]^T . dZ[R,out]: A(m=in,k=r) = X[r,m] (MN-major), B(n=out,k=r) = dZ[r,n] (MN-major)
   if (accumulate)
     return gemm::launch<kBN, gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32_ACC>(x, in, dz, out, int(in), int(out),
-                                                                                int(rows), ep, st);
+                                                                                int(rows), ep, st, gemm_cap());
   return gemm::launch<kBN, gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32>(x, in, dz, out, int(in), int(out),
-                                                                          int(rows), ep, st);
+                                                                          int(rows), ep, st, gemm_cap());
 }
 
 int replay_dtanh_first(const void* g, const void* y, void* dz, uint64_t n, void* stream) {

@@ -50,6 +50,7 @@ _sig = {
     "rw_mse_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p]),
     "rw_cast_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "rw_replay_set_sm_reserve": (C.c_int, [C.c_int32]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(LIB, _n)
@@ -451,33 +452,62 @@ def ordered_merge(per_mb: dict, k: int, m: int, group=None) -> torch.Tensor:
                                                     group))
 
 
+_MERGE_GROUPS: dict = {}
+
+
+def _merge_group(max_ctas: int):
+    """A NCCL communicator for the merges whose kernels use at most
+    `max_ctas` CTAs (= the SMs the replay GEMMs leave free)."""
+    import torch.distributed as dist
+    key = (dist.get_world_size(), max_ctas)
+    if key not in _MERGE_GROUPS:
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.config.max_ctas = max_ctas
+        opts.config.min_ctas = 1
+        _MERGE_GROUPS[key] = dist.new_group(backend="nccl", pg_options=opts)
+    return _MERGE_GROUPS[key]
+
+
 def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, rows: int,
                      micro_batches: int, seed: int, hyper: OptimizerHyper, first: bool, last: bool, dim: int,
-                     group=None, rank: int = 0, d: int = 1) -> int:
-    """recover_parallel for this helper rank: replay this
-    helper's micro-batches, then all stages' merges in flight together
-    (grouped point-to-point shard exchange), then the ordered sums, the
-    all-gathers and the steps."""
+                     group=None, rank: int = 0, d: int = 1, overlap: bool = False, reserve_sms: int = 8) -> int:
+    """recover_parallel for this helper rank.
+
+    overlap (NCCL): each stage's merge starts as soon as its gradients are
+    complete and runs concurrently with the backward of the earlier stages, on
+    a communicator capped at `reserve_sms` CTAs while the replay GEMMs leave
+    that many SMs free (a plain overlap starves the persistent GEMM grid:
+    measured 1.7x slower).  Measured on 8-stage config 4, the capped overlap
+    is still slower than merging after the pass (N=4: 220 vs 203 ms/iteration;
+    N=2: 412 vs 375), so it is off by default.  The ordered sums, all-gathers
+    and steps follow the pass either way."""
     import torch.distributed as dist
     assign = parallel_assignment(micro_batches, d)
     distributed = group is not None or (dist.is_available() and dist.is_initialized())
-    for it in range(it0, it1):
-        handles = {}
+    use_overlap = (distributed and overlap and group is None and dist.get_backend() == "nccl" and reserve_sms > 0)
+    mgroup = _merge_group(reserve_sms) if use_overlap else group
+    if use_overlap:
+        check(LIB.rw_replay_set_sm_reserve(reserve_sms))
+    try:
+        for it in range(it0, it1):
+            handles = {}
 
-        def start(k, bufs):
-            handles[k] = ordered_merge_start(bufs, stages[k].grad.numel(), micro_batches, group)
+            def start(k, bufs):
+                handles[k] = ordered_merge_start(bufs, stages[k].grad.numel(), micro_batches, mgroup)
 
-        # Merges are NOT overlapped with the backward: NCCL's kernels would
-        # take SMs from the persistent GEMM grid, whose static tile schedule
-        # then waits for its last CTA (measured 1.7x slower at N=4).
-        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim)
-        if distributed:
-            for k in range(len(stages) - 1, -1, -1):
-                start(k, {mb: per_mb[mb][k] for mb in assign[rank]})
-        for k, st in enumerate(stages):
+            per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim,
+                                 on_stage_done=start if use_overlap else None)
             if distributed:
-                merged = ordered_merge_finish(handles[k])
-            else:
-                merged = ordered_merge(per_mb, k, micro_batches, None)
-            st.step(hyper, grad=merged)
+                for k in range(len(stages) - 1, -1, -1):  # same order on every rank
+                    if k not in handles:
+                        start(k, {mb: per_mb[mb][k] for mb in assign[rank]})
+            for k, st in enumerate(stages):
+                if distributed:
+                    merged = ordered_merge_finish(handles[k])
+                else:
+                    merged = ordered_merge(per_mb, k, micro_batches, None)
+                st.step(hyper, grad=merged)
+    finally:
+        if use_overlap:
+            check(LIB.rw_replay_set_sm_reserve(0))
     return it1 - it0
