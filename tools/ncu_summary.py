@@ -1,6 +1,6 @@
 """Summarise ncu reports (gpurun_out/*.ncu-rep, launches.csv) into profiles/.
 
-usage: python tools/ncu_summary.py <key>=<report.ncu-rep> ... [--launches launches.csv]
+usage: python tools/ncu_summary.py <key>=<report.ncu-rep>[#launch] ... [--launches launches.csv]
                                    [--algo <key>=<bytes>] [--out profiles/ncu_summary.json]
 Writes/merges JSON keyed by <key> with the metrics the roofline needs
 (duration, dram bytes read/write, throughput %, registers, occupancy).
@@ -28,6 +28,7 @@ METRICS = {
     "sm__cycles_elapsed.avg.per_second": "sm_clock",
     "lts__t_bytes.sum": "l2_bytes",
     "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pct",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_active_pct",
     "sm__inst_executed_pipe_tma.sum": "tma_inst",
     "launch__func_name": "kernel",
     "Kernel Name": "kernel_name",
@@ -48,6 +49,8 @@ def raw(rep: str):
     for vals in rows[2:]:
         d = {}
         for i, h in enumerate(hdr):
+            if h.endswith("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"):
+                h = "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"
             if h in METRICS:
                 v = vals[i]
                 u = units[i] if i < len(units) else ""
@@ -64,6 +67,7 @@ def main():
     args = sys.argv[1:]
     out = Path("profiles/ncu_summary.json")
     algo = {}
+    flops = {}
     launches = None
     reps = []
     i = 0
@@ -82,17 +86,29 @@ def main():
             algo[k] = float(v)
             i += 2
             continue
+        if a == "--flops":
+            k, v = args[i + 1].split("=")
+            flops[k] = float(v)
+            i += 2
+            continue
         reps.append(a.split("=", 1))
         i += 1
     data = json.loads(out.read_text()) if out.exists() else {}
     for key, rep in reps:
+        idx = 0
+        if "#" in rep:  # report#launch-index
+            rep, idx = rep.split("#")
+            idx = int(idx)
         rs = raw(rep)
-        d = rs[0]
+        d = rs[idx]
         d["dram_bytes_per_launch"] = d.get("dram_read", 0) + d.get("dram_write", 0)
         if key in algo:
             d["algorithmic_bytes"] = algo[key]
             d["traffic_over_algorithmic"] = d["dram_bytes_per_launch"] / algo[key]
             d["achieved_algorithmic_gbs_under_ncu"] = algo[key] / d["duration"] / 1e9
+        if key in flops:
+            d["algorithmic_flops"] = flops[key]
+            d["achieved_tflops_under_ncu"] = flops[key] / d["duration"] / 1e12
         d["report"] = Path(rep).name
         data[key] = d
     if launches:
