@@ -229,6 +229,92 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def cpu_reference_recovery(undo_params_per_s: float, threads: int | None = None) -> dict:
+    """Config 3 on the host with the reference's own semantics (SURVEY §8d:
+    "host memcpy of the state", copy semantics SPEC:501): optimizer_undo of
+    the 290 updated GPT-2 XL groups at the measured block-parallel reference
+    rate + a copy of the resolved fp64 x, m, v (37.4 GB) at the measured
+    multi-threaded host memcpy rate.  Extrapolated from bounded samples (the
+    full fp64 state would need ~87 GB of host RAM)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from paper_2302_06173_b200.workloads import gpt2_xl_sizes
+    threads = threads or os.cpu_count() or 1
+    sizes = gpt2_xl_sizes()
+    undo_params = sum(sizes[len(sizes) // 2:])  # update order = reverse layers: the last 290 groups
+    n = 1 << 27  # 1 GiB of fp64 per buffer
+    src = np.random.default_rng(0).random(n)
+    dst = np.empty_like(src)
+    parts = np.array_split(np.arange(n), threads)
+
+    def cp(ix):
+        dst[ix[0]:ix[-1] + 1] = src[ix[0]:ix[-1] + 1]
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(cp, parts))
+        t0 = time.perf_counter()
+        list(ex.map(cp, parts))
+        dt = time.perf_counter() - t0
+    memcpy_gbs = n * 8 / dt / 1e9
+    state_bytes = sum(sizes) * 3 * 8
+    ms = (undo_params / undo_params_per_s + state_bytes / (memcpy_gbs * 1e9)) * 1e3
+    return dict(ms=round(ms, 1), undo_params=undo_params, undo_params_per_s=round(undo_params_per_s),
+                copy_bytes=state_bytes, memcpy_gbs=round(memcpy_gbs, 2), cores=threads, kind="reference",
+                sample="optimizer_undo rate from the bounded BERT-large sample + host memcpy of a 1 GiB "
+                       "fp64 buffer; extrapolated to GPT-2 XL")
+
+
+def cpu_reference_replay(seconds_target: float = 4.0, threads: int | None = None) -> dict:
+    """Config 4 on the host: the reference forward_stage + backward_stage
+    (oracle/_ref, fp64 triple loops) timed at a reduced shape (rows 256, a
+    512 -> 2048 -> 512 stage: the same 4x expansion), one independent stage
+    per thread, and extrapolated by FLOP count to the 8-stage config-4
+    iteration (a full-size CPU run is impractical)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import Ref
+    ref = Ref()
+    threads = threads or os.cpu_count() or 1
+    R, D, H = 256, 512, 2048
+    L = ref.L
+    stages = [L.ref_stage_make(3, D, H, D, 2, 7 + t) for t in range(threads)]
+    x = np.random.default_rng(1).random((R, D)) * 0.1
+    g = np.random.default_rng(2).random((R, D)) * 1e-3
+    from oracle.oracle import _dptr
+
+    import ctypes as C
+    shapes = [D * H, H, H * D, D]  # W0, b0, W1, b1 (the stage's blocks)
+
+    def one(si):
+        st = stages[si]
+        y = np.empty((R, D))
+        go = np.empty((R, D))
+        pg = [np.empty(k) for k in shapes]
+        parr = (C.POINTER(C.c_double) * len(pg))(*[_dptr(a) for a in pg])
+        if L.ref_forward_stage(st, _dptr(x), R, D, 0, _dptr(y)) or \
+                L.ref_backward_stage(st, _dptr(g), R, D, 0, _dptr(go), parr):
+            raise RuntimeError("reference stage call failed")
+    flop = 6 * R * (D * H + H * D)  # fwd + dgrad + wgrad per layer
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(one, range(threads)))  # warm-up
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < seconds_target:
+            list(ex.map(one, range(threads)))
+            n += threads
+        dt = time.perf_counter() - t0
+    for st in stages:
+        L.ref_stage_free(st)
+    gflops = flop * n / dt / 1e9
+    rows, dims, m, n_st = 16384, (4096, 16384, 4096), 8, 8
+    layer = [2 * rows * dims[0] * dims[1], 2 * rows * dims[1] * dims[2]]
+    flop_it = m * (n_st * 3 * sum(layer) - layer[0])
+    return dict(gflops=round(gflops, 2), ms_per_iteration=round(flop_it / (gflops * 1e9) * 1e3, 1),
+                cores=threads, kind="reference",
+                sample=f"forward_stage+backward_stage (oracle/_ref, fp64) on {n} stage-micro-batches of "
+                       f"{R}x{D}->{H}->{D}, one stage per thread; extrapolated by FLOPs to config 4")
+
+
 # --------------------------------------------------------------- B200 arm
 def _fill_adam_state(st, seed=2302):
     from paper_2302_06173_b200 import seeded_fill_
@@ -641,6 +727,11 @@ def run_b200(args) -> None:
             r = cpu_reference_undo(seconds_target=1.0, steps=3, warmup=1)
             cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
             cpu["params_per_s"] = r["params_per_s"]
+            if not args.no_extras:  # the same reference, for the recovery and replay extras
+                if "recovery" in extras:
+                    extras["recovery"]["cpu_reference"] = cpu_reference_recovery(r["params_per_s"])
+                if "replay" in extras:
+                    extras["replay"]["cpu_reference"] = cpu_reference_replay()
         except Exception as e:  # the oracle/_ref .so must have been built by build()
             cpu = {"value": None, "unit": "GB/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
