@@ -434,6 +434,91 @@ def pcie_probe(nbytes: int = 1 << 30) -> dict:
                 bidir_gbs_each=round(nbytes / tb / 1e9, 1))
 
 
+def config1_crash(reps: int = 40) -> dict:
+    """Config 1 as specified: SGDM on a 10M flat state in 100 groups, the
+    crash injected after half the groups were updated (MidUpdate(50), update
+    order = reverse group order); recovery = read markers + resolve + undo of
+    the 50 updated groups.  Device time of the undo (CUDA events) and wall time
+    of the whole resolution; the CPU reference runs optimizer_undo on the same
+    50 blocks of 100k params (oracle/_ref, fp64, 16 threads)."""
+    import numpy as np
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import SGDM as R_SGDM, Ref
+    from paper_2302_06173_b200 import SGDM, DeviceState, OptimizerHyper, seeded_fill_
+    from paper_2302_06173_b200.recovery import apply_resolution, resolve
+    from paper_2302_06173_b200.workloads import CONFIGS
+    sizes = CONFIGS["sgdm10m"]["sizes"]()
+    G = len(sizes)
+    st = DeviceState(sizes, kind=SGDM)
+    for i, t in enumerate((st.x, st.g, st.m)):
+        seeded_fill_(t, 40 + i)
+    h = OptimizerHyper(kind=SGDM, lr=0.1, momentum=0.9, dampening=0.0, weight_decay=1e-4)
+    dev_ms, wall_ms = [], []
+    for r in range(reps + 3):
+        st.write_markers([(10, 0)] * G)
+        st.step(h, stop_after=G // 2)                      # crash mid-update
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan = resolve(st.markers(), h, lens=sizes)
+        if r % 2:  # the API call (markers read + undo), wall time
+            apply_resolution(st, h, plan)
+            torch.cuda.synchronize()
+            if r >= 3:
+                wall_ms.append((time.perf_counter() - t0) * 1e3)
+            continue
+        order = [i for i in reversed(st.update_order()) if i in set(plan.undo_ids)]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st.undo(h, order)                                  # the undo launch alone, device time
+        e1.record()
+        torch.cuda.synchronize()
+        if r >= 3:
+            dev_ms.append(e0.elapsed_time(e1))
+    # the undo kernel alone (CUPTI activity record; the event-bracketed time
+    # above also contains the host-side preparation of the launch)
+    from torch.profiler import ProfilerActivity, profile
+    st.write_markers([(10, 0)] * G)
+    st.step(h, stop_after=G // 2)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        st.undo(h, list(range(G - 1, G // 2 - 1, -1)))
+        torch.cuda.synchronize()
+    kus = [(e.time_range.end - e.time_range.start) for e in prof.events()
+           if e.device_type.name == "CUDA" and "optim_kernel" in e.name]
+    undo_params = sum(sizes[G // 2:])
+    assert plan.strategy == "Undo" and len(plan.undo_ids) == G // 2
+    dm = statistics.median(dev_ms)
+    out = dict(workload="config 1: SGDM 10M flat fp32, 100 groups, crash after 50 (MidUpdate(50)), resolve + "
+                        "undo of the 50 updated groups",
+               undo_groups=G // 2, undo_params=undo_params, undo_call_device_ms=round(dm, 4),
+               undo_kernel_us=round(kus[0], 1) if kus else None,
+               undo_kernel_gbs=round(undo_params * 20 / (kus[0] * 1e-6) / 1e9, 1) if kus else None,
+               roofline_us=round(undo_params * 20 / (_peaks()["hbm_gbs"] * 1e9) * 1e6, 1),
+               resolve_plus_undo_wall_ms=round(statistics.median(wall_ms), 3))
+    del st
+    try:  # the same 50 blocks through the reference library
+        ref = Ref()
+        rh = dict(kind=R_SGDM, lr=0.1, momentum=0.9, dampening=0.0, weight_decay=1e-4)
+        blocks = []
+        for i in range(G // 2):
+            b = ref.block(sizes[i], seed=i)
+            b.set(m=np.full(sizes[i], 1e-3), t=10, updated=False)
+            b.step(np.full(sizes[i], 1e-3), rh)
+            blocks.append(b)
+        th = os.cpu_count() or 1
+        with ThreadPoolExecutor(th) as ex:
+            t0 = time.perf_counter()
+            list(ex.map(lambda b: b.undo(rh), blocks))
+            cpu_ms = (time.perf_counter() - t0) * 1e3
+        out["cpu_reference"] = dict(ms=round(cpu_ms, 2), cores=th, kind="reference",
+                                    sample="optimizer_undo of the same 50 x 100k blocks (fp64 as shipped)")
+    except Exception as e:  # pragma: no cover
+        out["cpu_reference"] = {"unavailable": str(e)[:200]}
+    return out
+
+
 def checkpoint_bench(sizes, reps: int = 2) -> dict:
     """Global checkpoint write + load of the config-2 Adam state (x, m, v fp32)
     through the native store: pinned pipelined D2H/H2D, GPU CRC32, fsync'd
@@ -691,6 +776,7 @@ def run_b200(args) -> None:
             msg = statistics.median(tsg)
             extras["sgdm10m_undo_all"] = dict(ms=round(msg, 4),
                                               gbs=round(nbsg / (msg * 1e-3) / 1e9, 1))
+            extras["config1_crash"] = config1_crash()
             # the other kinds of Table 1 on the same 336M BERT-large layout
             by_kind = {}
             for kn in ("sgd", "adamw", "lamb"):
