@@ -589,7 +589,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     if rank == 0:
         _fill_adam_state(st)
     out = {}
-    modes = ["nccl", "scatter_allgather", "fused", "auto"] if world > 1 else ["local"]
+    modes = ["nccl", "pipelined", "scatter_allgather", "fused", "auto"] if world > 1 else ["local"]
     for mode in modes:
         res = []
         kinfo = []
@@ -603,7 +603,8 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
             t_wall = time.perf_counter()
             plan = resolve(st.markers() if rank == 0 else [], h, lens=sizes if rank == 0 else None,
                            device=device)
-            if mode in ("auto", "scatter_allgather"):
+            t_resolved = time.perf_counter()
+            if mode in ("auto", "scatter_allgather", "pipelined"):
                 used, nbytes = recover(st, h, plan, src=0, transfer=mode)
                 kinfo.append({"used": used})
             elif mode == "fused":
@@ -618,13 +619,14 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
             torch.cuda.synchronize()
             wall = (time.perf_counter() - t_wall) * 1e3
             if it > 0:
-                res.append((wall, plan.strategy, plan.target, nbytes))
+                res.append((wall, plan.strategy, plan.target, nbytes, (t_resolved - t_wall) * 1e3))
         t = torch.tensor([statistics.median(r[0] for r in res)], device=device)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         nbytes = res[0][3]
-        out[mode] = dict(recovery_ms=round(ms, 3), strategy=res[0][1], target_iteration=res[0][2],
+        out[mode] = dict(recovery_ms=round(ms, 3), resolve_ms=round(statistics.median(r[4] for r in res), 3),
+                         strategy=res[0][1], target_iteration=res[0][2],
                          bytes_per_replacement=nbytes,
                          transfer_algbw_gbs=round(nbytes / (ms * 1e-3) / 1e9, 1) if nbytes else None,
                          frac_of_nvlink_roofline=round(nbytes / 770e9 / (ms * 1e-3), 3) if nbytes else None)

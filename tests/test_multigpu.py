@@ -99,6 +99,20 @@ def scen_fused(rank, world):
     recover_replication(st2, src=0)
     same_nccl = all(torch.equal(getattr(st2, n)[o:o + k].view(torch.int32), res[n][o:o + k].view(torch.int32))
                     for n in ("x", "m", "v") for o, k in zip(st.offsets, st.sizes))
+    # the pipelined path (undo run by run overlapped with async broadcasts) on a
+    # fresh torn copy gives the same bits on both ranks
+    from paper_2302_06173_b200.recovery import recover_replication_pipelined
+    st3 = DeviceState(sizes, kind=ADAM)
+    if rank == 0:
+        for i, t in enumerate((st3.x, st3.g, st3.m, st3.v)):
+            seeded_fill_(t, 40 + i)
+        st3.v.abs_()
+        st3.write_markers([(6, 0)] * len(sizes))
+        st3.step(h, stop_after=3)
+    recover_replication_pipelined(st3, h, plan, src=0, pieces=3)
+    same_pipe = all(torch.equal(getattr(st3, n)[o:o + k].view(torch.int32), res[n][o:o + k].view(torch.int32))
+                    for n in ("x", "m", "v") for o, k in zip(st.offsets, st.sizes))
+    same_pipe = same_pipe and st3.markers() == st.markers()
     diffs = {}
     if rank == 0:
         for n in ("x", "m", "v"):
@@ -106,7 +120,7 @@ def scen_fused(rank, world):
             bad = torch.nonzero(res[n].view(torch.int32) != getattr(twin, n).view(torch.int32))
             diffs[n] = (float(d.max()), int(bad.numel()), bad[:5].flatten().tolist())
     return dict(strategy=plan.strategy, ok_local=ok_local, same=all(same), same_list=same,
-                same_nccl=same_nccl, markers=st.markers(), nbytes=nb, diffs=diffs)
+                same_nccl=same_nccl, same_pipe=same_pipe, markers=st.markers(), nbytes=nb, diffs=diffs)
 
 
 @needs2
@@ -117,6 +131,7 @@ def test_fused_undo_push_bitexact():
     assert out[0]["ok_local"]
     assert out[0]["same"] and out[1]["same"]
     assert out[0]["same_nccl"] and out[1]["same_nccl"]
+    assert out[0]["same_pipe"] and out[1]["same_pipe"]
     assert out[0]["markers"] == out[1]["markers"] == [(6, 0)] * 6
 
 

@@ -17,6 +17,9 @@ from paper_2302_06173_b200.recovery import recover, recover_replication, resolve
 class HostState:
     def __init__(self, sizes, seed=None):
         n = sum(sizes)
+        self.sizes = list(sizes)
+        self.offsets = [sum(sizes[:i]) for i in range(len(sizes))]
+        self.num_groups = len(sizes)
         self.device = torch.device("cpu")
         g = torch.Generator().manual_seed(seed or 0)
         mk = (lambda: torch.randn(n, generator=g)) if seed is not None else (lambda: torch.zeros(n))
@@ -136,3 +139,28 @@ def test_scatter_allgather_world3():
             assert torch.equal(res[0][k].view(torch.int32), res[r][k].view(torch.int32))
         assert res[r]["mk"] == [(10, 0)] * 3
     assert all(res[r]["used"] == "scatter_allgather" for r in range(3))
+
+
+def scen_pipelined(rank):
+    """The pipelined transfer's run split and per-run broadcasts (no undo:
+    consistent markers) over gloo, world 3."""
+    h = OptimizerHyper(kind=ADAM)
+    sizes = [5, 7, 11, 3, 13, 2]
+    if rank == 0:
+        st = HostState(sizes, seed=21)
+        st.write_markers([(4, 0)] * len(sizes))
+        plan = resolve(st.markers(), h, lens=sizes)
+    else:
+        st = HostState(sizes)
+        plan = resolve([], h)
+    used, nbytes = recover(st, h, plan, src=0, transfer="pipelined")
+    return dict(used=used, strategy=plan.strategy, x=st.x.clone(), v=st.v.clone(), mk=st.markers(), nbytes=nbytes)
+
+
+def test_pipelined_transfer_world3():
+    res = _run(scen_pipelined, world=3)
+    assert res[0]["strategy"] == "None"
+    for r in (1, 2):
+        assert torch.equal(res[r]["x"], res[0]["x"]) and torch.equal(res[r]["v"], res[0]["v"])
+        assert res[r]["mk"] == [(4, 0)] * 6 and res[r]["used"] == "pipelined"
+    assert res[0]["nbytes"] == 41 * 4 * 3

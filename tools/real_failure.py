@@ -5,8 +5,8 @@
   dies (os._exit).  Rank 0 detects it from its stopped heartbeat, aborts the
   NCCL communicator, publishes the repair plan; a fresh replacement process
   claims rank 1's slot on the freed GPU; both join generation 1 over NCCL;
-  then resolve + recover (fused undo + NVLink push) hands the replacement the
-  resolved state, checked by device CRC32 of every buffer.
+  then resolve + recover (the undo pipelined with the NCCL transfer) hands the
+  replacement the resolved state, checked by device CRC32 of every buffer.
 
 Prints one JSON line: detection, repair and recovery times (ms).
   python tools/real_failure.py [gpt2xl|small]
@@ -42,7 +42,7 @@ def _crcs(st):
 def member(rank, port, which, q):
     from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper, seeded_fill_
     from paper_2302_06173_b200.membership import Membership, RepairPlan, abort_group, join_generation
-    from paper_2302_06173_b200.recovery import recover, resolve
+    from paper_2302_06173_b200.recovery import prepare_transfer, recover, resolve
     import datetime
     torch.cuda.set_device(rank)
     store = dist.TCPStore("127.0.0.1", port, is_master=False, timeout=datetime.timedelta(seconds=120))
@@ -69,6 +69,7 @@ def member(rank, port, which, q):
     mem.stop()
     join_generation(store, plan, rank, "nccl", device_id=torch.device("cuda", rank))
     dist.all_reduce(torch.zeros(1, device="cuda"))  # connect the new communicator
+    prepare_transfer(st)                            # and the transfer's per-buffer communicators
     torch.cuda.synchronize()
     t_join = time.time()
     p = resolve(st.markers(), h, lens=sizes)
@@ -87,7 +88,7 @@ def member(rank, port, which, q):
 def replacement(port, which, q):
     from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper
     from paper_2302_06173_b200.membership import claim_slot, join_generation
-    from paper_2302_06173_b200.recovery import recover, resolve
+    from paper_2302_06173_b200.recovery import prepare_transfer, recover, resolve
     import datetime
     store = dist.TCPStore("127.0.0.1", port, is_master=False, timeout=datetime.timedelta(seconds=120))
     sizes = _sizes(which)
@@ -100,6 +101,7 @@ def replacement(port, which, q):
     h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
     join_generation(store, plan, rank, "nccl", device_id=torch.device("cuda", rank))
     dist.all_reduce(torch.zeros(1, device="cuda"))
+    prepare_transfer(st)
     p = resolve([], h)
     used, nbytes = recover(st, h, p, src=0)
     torch.cuda.synchronize()
