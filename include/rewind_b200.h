@@ -192,6 +192,16 @@ int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* group
 int rw_ipc_export(const void* ptr, void* handle_out /*64 bytes*/, uint64_t* offset_out);
 int rw_ipc_import(const void* handle /*64 bytes*/, void** base_out);
 int rw_ipc_close(void* base);
+/* Copy-engine transfers between GPUs of one node (peer pointers from
+ * rw_ipc_import): n async device-to-device copies on `stream` (DMA engines,
+ * no kernels), and stream-ordered signalling through 64-bit epoch counters:
+ * write_u64 stores `value` at addr (a local or peer device address) after
+ * every prior operation of the stream has completed and is visible;
+ * wait_u64 blocks `stream` until *addr >= value. */
+int rw_copy_async(void* const* dsts, const void* const* srcs, const uint64_t* bytes, uint32_t n, void* stream);
+int rw_stream_write_u64(void* stream, void* addr, uint64_t value);
+int rw_stream_wait_u64(void* stream, const void* addr, uint64_t value);
+
 /* apply_undo fused with recover_replication: undoes undo_ids in place and, in
  * the same kernel, streams every group of the resolved state (x, m, v; g too
  * when peer_g != NULL) into the peer replica's buffers (same layout) with

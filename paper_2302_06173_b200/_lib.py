@@ -118,6 +118,9 @@ def _load() -> C.CDLL:
                                               P(rw_hyper), u32, dbl]),
         "rw_optimizer_undo_host": (C.c_int, [vp, P(rw_hyper), P(u32), u32, vp, vp, vp, vp, vp, vp, vp, u64,
                                              vp]),
+        "rw_copy_async": (C.c_int, [P(vp), P(vp), P(u64), u32, vp]),
+        "rw_stream_write_u64": (C.c_int, [vp, vp, u64]),
+        "rw_stream_wait_u64": (C.c_int, [vp, vp, u64]),
         "rw_state_saved_scalars": (C.c_int, [vp, u32, P(dbl), u32, P(u32), vp]),
         "rw_state_set_saved_scalars": (C.c_int, [vp, u32, P(dbl), u32, vp]),
     }

@@ -468,23 +468,34 @@ def _merge_group(max_ctas: int):
     return _MERGE_GROUPS[key]
 
 
+_CE_MERGERS: dict = {}
+
+
 def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, rows: int,
                      micro_batches: int, seed: int, hyper: OptimizerHyper, first: bool, last: bool, dim: int,
-                     group=None, rank: int = 0, d: int = 1, overlap: bool = False, reserve_sms: int = 8) -> int:
+                     group=None, rank: int = 0, d: int = 1, merge: str = "auto", overlap: bool = False,
+                     reserve_sms: int = 8) -> int:
     """recover_parallel for this helper rank.
 
-    overlap (NCCL): each stage's merge starts as soon as its gradients are
-    complete and runs concurrently with the backward of the earlier stages, on
-    a communicator capped at `reserve_sms` CTAs while the replay GEMMs leave
-    that many SMs free (a plain overlap starves the persistent GEMM grid:
-    measured 1.7x slower).  Measured on 8-stage config 4, the capped overlap
-    is still slower than merging after the pass (N=4: 220 vs 203 ms/iteration;
-    N=2: 412 vs 375), so it is off by default.  The ordered sums, all-gathers
-    and steps follow the pass either way."""
+    merge="copy_engine" (auto with NCCL on one node): each stage's shards leave
+    over the DMA engines as soon as its gradients are complete, overlapping the
+    backward of the earlier stages without taking SMs from the GEMMs
+    (merge.CopyEngineMerger); the ordered sums, the gather and the steps follow.
+    merge="nccl": grouped point-to-point exchange after the pass (or, with
+    overlap=True, during it on a communicator capped at `reserve_sms` CTAs
+    while the GEMMs leave that many SMs free: measured slower, N=4 220 vs
+    203 ms/iteration).  Every path sums in ascending micro-batch order, so all
+    are bit-identical to the sequential replay."""
     import torch.distributed as dist
     assign = parallel_assignment(micro_batches, d)
     distributed = group is not None or (dist.is_available() and dist.is_initialized())
-    use_overlap = (distributed and overlap and group is None and dist.get_backend() == "nccl" and reserve_sms > 0)
+    nccl = distributed and dist.get_backend(group) == "nccl"
+    if merge == "auto":
+        merge = "copy_engine" if (nccl and dist.get_world_size(group) <= torch.cuda.device_count()) else "nccl"
+    if distributed and merge == "copy_engine":
+        return _recover_parallel_ce(stages, log, it0, it1, rows, micro_batches, seed, hyper, first, last, dim,
+                                    group, rank, assign)
+    use_overlap = (nccl and overlap and group is None and reserve_sms > 0)
     mgroup = _merge_group(reserve_sms) if use_overlap else group
     if use_overlap:
         check(LIB.rw_replay_set_sm_reserve(reserve_sms))
@@ -510,4 +521,34 @@ def recover_parallel(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: i
     finally:
         if use_overlap:
             check(LIB.rw_replay_set_sm_reserve(0))
+    return it1 - it0
+
+
+def _recover_parallel_ce(stages, log, it0, it1, rows, micro_batches, seed, hyper, first, last, dim, group, rank,
+                         assign) -> int:
+    from .merge import CopyEngineMerger
+    import torch.distributed as dist
+    key = (tuple(st.grad.numel() for st in stages), micro_batches, dist.get_world_size(group), id(group))
+    if key not in _CE_MERGERS:
+        _CE_MERGERS[key] = CopyEngineMerger(key[0], micro_batches, group)
+    mg = _CE_MERGERS[key]
+    for it in range(it0, it1):
+        mg.begin_iteration()
+        pending = {}
+
+        def ship(k, bufs):
+            # scatter + (queued behind the peers' counters) reduce and gather of
+            # stage k, overlapping the backward of stages k-1..0
+            mg.scatter(k, bufs)
+            pending[k] = mg.reduce_gather(k, bufs, wait=False)
+
+        per_mb = helper_pass(stages, log, it, assign[rank], rows, micro_batches, seed, first, last, dim,
+                             on_stage_done=ship)
+        for k in range(len(stages) - 1, -1, -1):  # a helper without micro-batches still signals
+            if k not in pending:
+                ship(k, {mb: per_mb[mb][k] for mb in assign[rank]})
+        for k, st in enumerate(stages):
+            merged, ev = pending[k]
+            torch.cuda.current_stream().wait_event(ev)
+            st.step(hyper, grad=merged)
     return it1 - it0
