@@ -305,3 +305,39 @@ def test_undo_from_host_pipelined_equals_device_undo(kind):
     with pytest.raises(RwError) as e:  # guards before any copy
         st.undo_from_host(h, host, out, ids=[0])
     assert e.value.name == "NothingToUndo"
+
+
+@pytest.mark.parametrize("cfg", ["adam340m", "adam1b"])
+def test_full_size_configs_sampled_bitexact(restate, cfg):
+    """The BASELINE sizes themselves (config 2 BERT-large 336M in 398 groups;
+    the north-star 1B in 250 groups): step then undo in one launch each, every
+    sampled element bit-identical to the fp32 restatement (elementwise ops, so
+    sampling is exact), every marker as optimizer_step/undo leave it, and no
+    non-finite value anywhere."""
+    from paper_2302_06173_b200.workloads import CONFIGS
+    sizes = CONFIGS[cfg]["sizes"]()
+    st = DeviceState(sizes, kind=ADAM)
+    seeded_fill_(st.x, 11)
+    seeded_fill_(st.m, 12)
+    st.m.mul_(0.01)
+    seeded_fill_(st.v, 13)
+    st.v.abs_().mul_(1e-4)
+    seeded_fill_(st.g, 14)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    n = 1 << 20
+    idx = torch.randint(0, st.total, (n,), device="cuda", generator=gen)
+    x0, g0, m0, v0 = (getattr(st, k)[idx].cpu().numpy() for k in ("x", "g", "m", "v"))
+    st.write_markers([(20, 0)] * len(sizes))
+    h = HYP[ADAM]
+    st.step(h)
+    st.check_finite()
+    assert st.markers() == [(21, 1)] * len(sizes)
+    rx, rm, rv, _ = restate.step(ADAM, h, 20, x0, g0, m0, v0, dtype=np.float32)
+    assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(rx))
+    assert np.array_equal(_bits(st.m[idx].cpu().numpy()), _bits(rm))
+    st.undo(h)
+    st.check_finite()
+    assert st.markers() == [(20, 0)] * len(sizes)
+    ux, um, uv, _ = restate.undo(ADAM, h, 21, rx, g0, rm, rv, dtype=np.float32)
+    assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(ux))
+    assert np.array_equal(_bits(st.v[idx].cpu().numpy()), _bits(uv))
