@@ -519,6 +519,70 @@ def config1_crash(reps: int = 40) -> dict:
     return out
 
 
+def config5_sweep(m: int = 8) -> dict:
+    """Config 5: selective-logging sweep on a Llama-7B-shaped pipeline (p = 8
+    stages of 4 MLP blocks 4096 -> 11008 -> 4096 = 8 affine+tanh layers,
+    micro-batch 8 x 2048 = 16384 rows).  "Log every k-th stage boundary"
+    (uniform groups of k stages): for k in {1, 2, 4, 8} the log
+    bytes per iteration = (p/k - 1) boundaries x m x (activation + gradient),
+    and the replay of one failed group per lost iteration is measured on the
+    tcgen05 path (group [0, k): its inputs are re-derived, its output gradient
+    logged unless k = p).  The SPEC planner (group_machines /
+    recovery_time_estimate) then runs on the measured per-stage
+    replay time."""
+    import torch
+
+    from paper_2302_06173_b200 import ADAM, OptimizerHyper, planner
+    from paper_2302_06173_b200.replay import BoundaryLog, Stage, replay_group, synth_inputs
+    p, R, H, F, blocks = 8, 16384, 4096, 11008, 4
+    dims = [H, F] * blocks + [H]
+    L = len(dims) - 1
+    h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
+    layer = [2 * R * dims[i] * dims[i + 1] for i in range(L)]
+    boundary_bytes = R * H * 2
+    res = {"p": p, "rows": R, "micro_batches": m, "stage_dims": dims, "sweep": []}
+    for k in (1, 2, 4, 8):
+        torch.cuda.empty_cache()
+        stages = [Stage(s, H, F, H, L, 7, ADAM, dims=dims) for s in range(k)]
+        last = k == p
+        log = BoundaryLog()
+        if not last:
+            for mb in range(m):
+                g = synth_inputs(9, 0, mb, R, H).mul_(1e-3)
+                for it in range(2):
+                    log.grads[(it, mb)] = g
+        replay_group(stages, log, 0, 1, R, m, 7, h, first=True, last=last, dim=H)  # warm-up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        replay_group(stages, log, 1, 2, R, m, 7, h, first=True, last=last, dim=H)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        flop = m * (k * 3 * sum(layer) - layer[0])  # the group's first layer needs no dgrad
+        nb = p // k - 1
+        res["sweep"].append(dict(k=k, groups=p // k, logged_boundaries=nb,
+                                 log_bytes_per_iteration=nb * m * 2 * boundary_bytes,
+                                 replay_ms_per_lost_iteration=round(ms, 2),
+                                 replay_tflops=round(flop / (ms * 1e-3) / 1e12, 1)))
+        del stages, log
+    torch.cuda.empty_cache()
+    r1 = res["sweep"][0]["replay_ms_per_lost_iteration"] / 1e3
+    M = [m * 2 * boundary_bytes] * (p - 1)
+    B, T = 25e9, 100
+    plans = []
+    for frac in (1.0, 0.5, 0.25, 0.0):
+        Mmax = frac * T * sum(M)
+        for par in (False, True):
+            gp = planner.group_machines([r1] * p, M, B, T, Mmax, parallel=par)
+            plans.append(dict(M_max_fraction=frac, parallel=par, groups=gp.groups, storage_bytes=gp.storage,
+                              est_recovery_s_per_lost_iteration=round(gp.recovery, 4),
+                              est_recovery_s_50_lost=round(
+                                  planner.recovery_time_estimate([r1] * p, M, B, gp.groups, 50, par), 3)))
+    res["planner"] = dict(R_stage_s=r1, boundary_bytes_per_iteration=M[0], B=B, T=T, plans=plans)
+    return res
+
+
 def checkpoint_bench(sizes, reps: int = 2) -> dict:
     """Global checkpoint write + load of the config-2 Adam state (x, m, v fp32)
     through the native store: pinned pipelined D2H/H2D, GPU CRC32, fsync'd
@@ -789,6 +853,11 @@ def run_b200(args) -> None:
                 by_kind[kn] = dict(undo_ms=round(mk_, 4), undo_gbs=round(nbk / (mk_ * 1e-3) / 1e9, 1),
                                    step_ms=round(statistics.median(measure_undo.last_step_ms), 4))
             extras["undo_by_kind_340m"] = by_kind
+            try:
+                extras["config5_sweep"] = config5_sweep()
+            except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
+                extras["config5_sweep"] = {"error": f"OOM: {e}"}
+            torch.cuda.empty_cache()
             try:
                 extras["checkpoint"] = checkpoint_bench(sizes)
             except Exception as e:  # pragma: no cover - disk space / permissions on the box
