@@ -378,12 +378,19 @@ bool parse_global_manifest(const std::string& text, uint64_t it, uint32_t* worke
   return true;
 }
 
+int first_device_blob(const rw_blob* blobs, uint32_t n) {
+  for (uint32_t i = 0; blobs && i < n; ++i)
+    if (!blobs[i].on_host && blobs[i].bytes) return rwb::DeviceScope::device_of(blobs[i].data);
+  return -1;
+}
+
 }  // namespace
 
 extern "C" {
 
 int rw_ckpt_write(const char* dir, uint64_t iteration, uint32_t worker, const rw_blob* blobs, uint32_t n,
                   uint32_t crash_after_blobs, void* stream) {
+  rwb::DeviceScope dev_scope(first_device_blob(blobs, n));
   if (!dir || (n && !blobs)) return cfail(RW_INVALID_ARGUMENT, "null argument");
   for (uint32_t i = 0; i < n; ++i) {
     if (!valid_name(blobs[i].name)) return cfail(RW_INVALID_ARGUMENT, "blob names are [A-Za-z0-9._-]+");
@@ -498,6 +505,7 @@ int rw_ckpt_blob_bytes(const char* dir, uint64_t iteration, uint32_t worker, con
 
 int rw_ckpt_load(const char* dir, uint64_t iteration, uint32_t worker, const rw_blob* blobs, uint32_t n,
                  void* stream) {
+  rwb::DeviceScope dev_scope(first_device_blob(blobs, n));
   if (!dir || (n && !blobs)) return cfail(RW_INVALID_ARGUMENT, "null argument");
   std::string text;
   uint32_t workers = 0;

@@ -1,6 +1,8 @@
 // Internal declarations shared by the CUDA kernels and the C-ABI host code.
 // Not part of the public boundary (see include/rewind_b200.h).
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 #include "rewind_b200.h"
@@ -57,6 +59,49 @@ struct LaunchArgs {
   void* pg = nullptr;
   void* pm = nullptr;
   void* pv = nullptr;
+};
+
+// Kernel attributes (max dynamic smem) are per device: true the first time a
+// call site runs on the current device (mask bit per device index).
+inline bool first_on_device(unsigned long long& mask) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long b = 1ull << (d & 63);
+  if (mask & b) return false;
+  mask |= b;
+  return true;
+}
+
+// The CUDA runtime is shared with the caller (PyTorch), whose current device
+// may differ from the memory an entry point works on (PyTorch sets devices
+// lazily).  Every entry point that launches work binds the device of the state
+// / the caller's memory for its duration and restores the caller's device.
+class DeviceScope {
+ public:
+  explicit DeviceScope(int dev) { bind(dev); }
+  ~DeviceScope() {
+    if (changed_) cudaSetDevice(prev_);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+  // device of a device pointer, or -1 for host / unknown memory
+  static int device_of(const void* p) {
+    if (!p) return -1;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return -1;
+    }
+    return (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? a.device : -1;
+  }
+
+ private:
+  void bind(int dev) {
+    if (dev < 0 || cudaGetDevice(&prev_) != cudaSuccess || prev_ == dev) return;
+    changed_ = cudaSetDevice(dev) == cudaSuccess;
+  }
+  int prev_ = 0;
+  bool changed_ = false;
 };
 
 // record the thread-local last-error message (rw_last_error_message)

@@ -142,16 +142,16 @@ __global__ void __launch_bounds__(kCrcThreads) crc_final_kernel(const uint8_t* _
 struct CrcOps {
   TreeOps tree;
   Mat chunk;
-  bool ready = false;
 };
+CrcOps make_crc_ops() {
+  CrcOps ops;
+  const Mat b = op_one_byte();
+  for (int l = 0; l < kLevels; ++l) ops.tree.op[l] = op_pow(b, uint64_t(kPiece) << l);
+  ops.chunk = op_pow(b, kChunk);
+  return ops;
+}
 const CrcOps& crc_ops() {
-  static CrcOps ops;
-  if (!ops.ready) {
-    const Mat b = op_one_byte();
-    for (int l = 0; l < kLevels; ++l) ops.tree.op[l] = op_pow(b, uint64_t(kPiece) << l);
-    ops.chunk = op_pow(b, kChunk);
-    ops.ready = true;
-  }
+  static const CrcOps ops = make_crc_ops();  // thread-safe one-time init
   return ops;
 }
 
@@ -162,12 +162,11 @@ int launch_crc32(const void* data, uint64_t n, uint32_t* out_dev, uint32_t* scra
   auto st = static_cast<cudaStream_t>(stream);
   const CrcOps& ops = crc_ops();
   const uint64_t nchunks = n / kChunk;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long dev_mask = 0;
+  if (first_on_device(dev_mask)) {
     const cudaError_t e = cudaFuncSetAttribute(crc_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                static_cast<int>(kChunk));
     if (e != cudaSuccess) return static_cast<int>(e);
-    attr = true;
   }
   if (nchunks) {
     crc_chunks_kernel<<<static_cast<unsigned>(nchunks), kCrcThreads, kChunk, st>>>(

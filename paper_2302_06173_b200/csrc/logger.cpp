@@ -191,6 +191,7 @@ void committer(rw_logger* L) {
 extern "C" {
 
 int rw_crc32_device(const void* data, uint64_t n, uint32_t* out_dev, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(data));
   if ((!data && n) || !out_dev) return lfail(RW_INVALID_ARGUMENT, "null argument");
   uint32_t* scratch = nullptr;
   LCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), rwb::crc32_scratch_words(n) * 4,
@@ -237,6 +238,7 @@ int rw_logger_create(rw_logger** out, const char* dir, uint32_t machine, uint32_
 }
 
 int rw_logger_log(rw_logger* L, const rw_log_record* rec, const void* dev_payload, void* producer_stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(dev_payload));
   if (!L || !rec || (!dev_payload && rec->payload_bytes)) return lfail(RW_INVALID_ARGUMENT, "null argument");
   if (rec->ndim > 4) return lfail(RW_INVALID_SHAPE, "InvalidShape: ndim > 4");
   if (L->err) return lfail(L->err, L->errmsg);

@@ -529,9 +529,10 @@ template <typename T, int KIND, bool UNDO, bool COPY_GRAD, bool PUSH = false>
 int launch_t(const LaunchArgs& a, cudaStream_t st) {
   auto kern = optim_kernel<T, KIND, UNDO, COPY_GRAD, PUSH>;
   constexpr size_t smem = dyn_smem_bytes<T, KIND>();
-  static int blocks_per_sm = -1;  // per instantiation
+  static int blocks_per_sm = -1;  // per instantiation (same on every B200)
   static int num_sms = -1;
-  if (blocks_per_sm < 0) {
+  static unsigned long long dev_mask = 0;
+  if (first_on_device(dev_mask)) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);

@@ -35,6 +35,7 @@ F entry(const char* name) {
 extern "C" {
 
 int rw_copy_async(void* const* dsts, const void* const* srcs, const uint64_t* bytes, uint32_t n, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of((n && srcs) ? srcs[0] : nullptr));
   if (n && (!dsts || !srcs || !bytes)) return pfail(RW_INVALID_ARGUMENT, "null argument");
   auto cs = static_cast<cudaStream_t>(stream);
   for (uint32_t i = 0; i < n; ++i) {

@@ -35,6 +35,7 @@ int check_desc(const rw_stage_desc* st, int64_t rows) {
 extern "C" {
 
 int rw_stage_forward(const rw_stage_desc* st, int64_t rows, void* const* acts, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(acts ? acts[0] : nullptr));
   int s = check_desc(st, rows);
   if (s) return s;
   if (!acts) return rfail(RW_INVALID_ARGUMENT, "null activations");
@@ -57,6 +58,7 @@ int rw_stage_backward(const rw_stage_desc* st, int64_t rows, void* const* acts, 
 int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
                          int32_t grad_in_is_dz, void* grad_out, const void* prev_y, float* const* dw,
                          float* const* db, int32_t accumulate, void* dz0, void* dz1, float* scratch, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(grad_in));
   int s = check_desc(st, rows);
   if (s) return s;
   if (!acts || !grad_in || !dw || !db || !dz0 || !dz1 || !scratch)
@@ -102,6 +104,7 @@ int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* act
 
 int rw_mse_grad(const void* pred, const float* target, uint64_t n, uint64_t micro_batches, void* grad, double* loss,
                 double* scratch, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(pred));
   if (micro_batches == 0) return rfail(RW_INVALID_CONFIG, "InvalidConfig: micro_batches must be >= 1");
   if (!pred || !target || !grad || !scratch) return rfail(RW_INVALID_ARGUMENT, "null argument");
   int e = rwb::replay_mse_grad(pred, target, n, micro_batches, grad, loss, scratch, stream);
@@ -112,6 +115,7 @@ int rw_mse_grad(const void* pred, const float* target, uint64_t n, uint64_t micr
 int rw_replay_set_sm_reserve(int32_t n) { return rwb::replay_set_sm_reserve(n); }
 
 int rw_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(in));
   if (!in || !out) return rfail(RW_INVALID_ARGUMENT, "null argument");
   int e = rwb::replay_cast_bf16(in, out, n, stream);
   if (e) return cfail(e, "cast");

@@ -374,6 +374,7 @@ int rw_lr_at(const rw_hyper* h, uint64_t t, double* out) {
 
 int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v, void* vmax,
                     uint64_t total, const rw_group* groups, uint32_t n_groups, int32_t device) {
+  rwb::DeviceScope dev_scope(device);
   if (!out) return fail(RW_INVALID_ARGUMENT, "null out");
   *out = nullptr;
   if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "dtype must be RW_F32 or RW_F64");
@@ -421,6 +422,7 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
 }
 
 void rw_state_destroy(rw_state* s) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s) return;
   cudaSetDevice(s->device);
   for (auto& sl : s->slots) {
@@ -459,6 +461,7 @@ void* rw_state_ptr(rw_state* s, int which) {
 
 int rw_state_saved_scalars(rw_state* s, uint32_t group, double* out, uint32_t cap, uint32_t* count,
                            void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s || !count || (cap && !out)) return fail(RW_INVALID_ARGUMENT, "null argument");
   if (group >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", group);
   const uint32_t c = s->trust_count[group];
@@ -475,6 +478,7 @@ int rw_state_saved_scalars(rw_state* s, uint32_t group, double* out, uint32_t ca
 }
 
 int rw_state_set_saved_scalars(rw_state* s, uint32_t group, const double* in, uint32_t count, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s || (count && !in)) return fail(RW_INVALID_ARGUMENT, "null argument");
   if (group >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", group);
   if (count > kTrustDepth) return fail(RW_TOO_LARGE, "TooLarge: at most %u saved scalars per group", kTrustDepth);
@@ -490,6 +494,7 @@ int rw_state_set_saved_scalars(rw_state* s, uint32_t group, const double* in, ui
 }
 
 int rw_state_read_groups(rw_state* s, rw_group* out, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s || !out) return fail(RW_INVALID_ARGUMENT, "null argument");
   if (s->mirror.empty()) return RW_OK;
   RW_CUDA(cudaSetDevice(s->device));
@@ -505,6 +510,7 @@ int rw_state_read_groups(rw_state* s, rw_group* out, void* stream) {
 }
 
 int rw_state_write_groups(rw_state* s, const rw_group* in, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s || !in) return fail(RW_INVALID_ARGUMENT, "null argument");
   if (s->mirror.empty()) return RW_OK;
   for (size_t i = 0; i < s->mirror.size(); ++i) {
@@ -521,6 +527,7 @@ int rw_state_write_groups(rw_state* s, const rw_group* in, void* stream) {
 }
 
 int rw_state_check(rw_state* s, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s) return fail(RW_INVALID_ARGUMENT, "null state");
   if (s->mirror.empty()) return RW_OK;
   std::vector<rw_group> dev(s->mirror.size());
@@ -542,6 +549,7 @@ int rw_state_check(rw_state* s, void* stream) {
 }
 
 int rw_clear_updated(rw_state* s, const uint32_t* ids, uint32_t n, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s) return fail(RW_INVALID_ARGUMENT, "null state");
   for (uint32_t i = 0; i < n; ++i) {
     if (ids[i] >= s->mirror.size()) return fail(RW_INVALID_ARGUMENT, "group id %u out of range", ids[i]);
@@ -556,6 +564,7 @@ int rw_clear_updated(rw_state* s, const uint32_t* ids, uint32_t n, void* stream)
 // optimizer_step, optim.cpp:338-364
 int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n,
                       const void* grad, uint32_t stop_after, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s || !h || (n && !ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
   if (n > stop_after) n = stop_after;  // MidUpdate(k): the crash hits after k groups
   std::vector<double> etas(n);
@@ -651,6 +660,7 @@ extern "C" {
 
 // optimizer_undo, optim.cpp:366-385 and the per-kind guards of undo_<kind>
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   std::vector<double> etas;
   int st = undo_prepare(s, h, ids, n, etas, stream);
   if (st) return st;
@@ -665,6 +675,7 @@ int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint3
 int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, const void* hx,
                            const void* hg, const void* hm, const void* hv, void* ox, void* om, void* ov,
                            uint64_t slice_elems, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   std::vector<double> etas;
   int st = undo_prepare(s, h, ids, n, etas, stream);
   if (st) return st;
@@ -826,6 +837,7 @@ uint64_t rw_derive_seed(uint64_t base, const uint64_t* parts, uint32_t n) {  // 
   return h;
 }
 int rw_seeded_fill(int32_t dtype, void* out, uint64_t n, uint64_t seed, uint64_t offset, void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(out));
   if (!out && n) return fail(RW_INVALID_ARGUMENT, "null out");
   int e = rwb::launch_seeded_fill(dtype, out, n, seed, offset, stream);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "seeded_fill");
@@ -833,6 +845,7 @@ int rw_seeded_fill(int32_t dtype, void* out, uint64_t n, uint64_t seed, uint64_t
 }
 int rw_ordered_sum(int32_t dtype, const void* const* tensors, uint32_t count, uint64_t n, void* out,
                    void* stream) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(out));
   if (count == 0) return fail(RW_EMPTY_INPUT, "EmptyInput: ordered_sum of nothing");
   int e = rwb::launch_ordered_sum(dtype, tensors, count, n, out, stream);
   if (e) return cuda_fail(static_cast<cudaError_t>(e), "ordered_sum");
@@ -1067,6 +1080,7 @@ AddrRangeFn addr_range_fn() {
 extern "C" {
 
 int rw_ipc_export(const void* ptr, void* handle_out, uint64_t* offset_out) {
+  rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(ptr));
   if (!ptr || !handle_out || !offset_out) return fail(RW_INVALID_ARGUMENT, "null argument");
   AddrRangeFn fn = addr_range_fn();
   if (!fn) return fail(RW_CUDA_ERROR, "cuMemGetAddressRange unavailable");
@@ -1099,6 +1113,7 @@ int rw_ipc_close(void* base) {
 // resolved state (x, m, v; g when peer_g) into a peer replica over NVLink.
 int rw_undo_and_push(rw_state* s, const rw_hyper* h, const uint32_t* undo_ids, uint32_t n_undo, void* peer_x,
                      void* peer_g, void* peer_m, void* peer_v, void* stream) {
+  rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s || !h || !peer_x || (n_undo && !undo_ids)) return fail(RW_INVALID_ARGUMENT, "null argument");
   const bool um = h->kind != RW_SGD, uv = h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB;
   if ((um && !peer_m) || (uv && !peer_v)) return fail(RW_INVALID_ARGUMENT, "peer m/v buffers required");

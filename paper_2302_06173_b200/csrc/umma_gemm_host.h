@@ -55,12 +55,14 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
   e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN) : make_map(&mb, B, K, N, ldb, 64);
   if (e) return e;
   auto kern = umma_gemm_kernel<BN, AMAJ, BMAJ, EPI>;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long dev_mask = 0;  // the attribute is per device
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  if (!(dev_mask & (1ull << (cur_dev & 63)))) {
     cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(Cfg<BN>::kSmem));
     if (ce != cudaSuccess) return static_cast<int>(ce);
-    attr = true;
+    dev_mask |= 1ull << (cur_dev & 63);
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -82,12 +84,14 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
   e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN / 2) : make_map(&mb, B, K, N, ldb, 64);
   if (e) return e;
   auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI>;
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long dev_mask = 0;  // the attribute is per device
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  if (!(dev_mask & (1ull << (cur_dev & 63)))) {
     cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(Cfg2<BN>::kSmem));
     if (ce != cudaSuccess) return static_cast<int>(ce);
-    attr = true;
+    dev_mask |= 1ull << (cur_dev & 63);
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -179,3 +179,30 @@ def test_parallel_replay_two_ranks_bitexact():
     for r in (0, 1):
         assert out[r]["eq_seq"] and out[r]["eq_ghost"]
         assert out[r]["eq_group"]
+
+
+@needs2
+def test_two_devices_in_one_process():
+    """Per-device kernel attributes: the fused kernels, the CRC and the GEMMs
+    launched on cuda:0 and then on cuda:1 from the same process."""
+    from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper, seeded_fill_
+    from paper_2302_06173_b200.logstore import crc32_device
+    h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
+    outs = []
+    for d in (0, 1):
+        with torch.cuda.device(d):
+            st = DeviceState([70_001, 3_000], kind=ADAM, device=d)
+            for i, n in enumerate(("x", "g", "m", "v")):
+                seeded_fill_(getattr(st, n), 5 + i)
+            st.v.abs_()
+            st.step(h)
+            st.undo(h)
+            st.check_finite()
+            outs.append((st.x.cpu(), crc32_device(st.x.view(torch.uint8))))
+            from paper_2302_06173_b200.replay import Stage
+            sg = Stage(0, 64, 128, 64, 2, 3, ADAM, device=d)
+            acts = sg.new_acts(128)
+            acts[0].normal_()
+            sg.forward(acts)
+            torch.cuda.synchronize(d)
+    assert torch.equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
