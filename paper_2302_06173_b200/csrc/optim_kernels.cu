@@ -225,7 +225,11 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 constexpr int kThreads = 256;
-constexpr int kStages = 3;
+constexpr int kStages = 3;      // smem stages; 2 CTAs per SM
+// fused NVLink push: 4 stages (2 tiles of stores in flight, 1 CTA per SM)
+// measured no faster than 3 (GPT-2 XL push 29.8 vs 29.9 ms), so 3
+constexpr int kStagesPush = 3;
+constexpr int kStagesMax = 4;
 constexpr uint32_t kSlotBytes = 8192;  // per stream per stage
 
 // per-stage tile descriptor, written by the producer thread before it arms
@@ -245,9 +249,13 @@ struct StageMeta {
   ScalarSet ss;    // eta, c1, c2, denom of the tile's group
 };
 
-template <typename T, int KIND>
+template <bool PUSH>
+constexpr int stages_for() {
+  return PUSH ? kStagesPush : kStages;
+}
+template <typename T, int KIND, bool PUSH>
 constexpr size_t dyn_smem_bytes() {
-  return size_t(kStages) * Uses<KIND>::slots * kSlotBytes;
+  return size_t(stages_for<PUSH>()) * Uses<KIND>::slots * kSlotBytes;
 }
 
 // PUSH: the resolved tiles are also written to a peer replica (NVLink stores
@@ -269,8 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
   constexpr int SX = 0, SG = 1, SM = 2, SV = 3, SW = 4;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  __shared__ uint64_t full[kStages];
-  __shared__ StageMeta meta[kStages];
+  constexpr int S = stages_for<PUSH>();
+  constexpr int D = S - 2;  // tiles whose stores may still be in flight
+  __shared__ uint64_t full[kStagesMax];
+  __shared__ StageMeta meta[kStagesMax];
   T* const buf = reinterpret_cast<T*>(smem_raw);
   auto slot = [&](int st, int k) { return buf + (size_t(st) * NS + k) * TILE; };
   const T* gsrc = COPY_GRAD ? grad : g;
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
   };
 
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (c_begin < c_end) {
       uint32_t lo = 0, hi = n_work;
@@ -387,17 +397,17 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
   };
 
   if (tid == 0) {
-    for (int k = 0; k < kStages; ++k) {
+    for (int k = 0; k < S; ++k) {
       const uint32_t c = c_begin + uint32_t(k);
       if (c < c_end) issue(c, k);
     }
   }
 
-  uint32_t prev_item = 0, prev_chunk = 0;
+  uint32_t ring_item[D], ring_chunk[D];  // the last D tiles (thread 0)
   uint32_t iter = 0;
   for (uint32_t chunk = c_begin; chunk < c_end; ++chunk, ++iter) {
-    const int st = static_cast<int>(iter % kStages);
-    mbar_wait(&full[st], (iter / kStages) & 1u);
+    const int st = static_cast<int>(iter % S);
+    mbar_wait(&full[st], (iter / S) & 1u);
     const StageMeta& mt = meta[st];
     s.eta = A::cvt(mt.ss.eta);
     s.c1 = A::cvt(mt.ss.c1);
@@ -508,19 +518,20 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
       bulk_commit();
       if (mt.bad) atomicOr(&groups[mt.gid].flags, 1u);
       const uint32_t this_item = mt.item;
-      if (iter > 0) {
-        bulk_wait<1>();  // the previous tile's stores are complete
-        account(prev_item);
-        const uint32_t nc = prev_chunk + uint32_t(kStages);
-        if (nc < c_end) issue(nc, static_cast<int>((iter - 1) % kStages));
+      if (iter >= uint32_t(D)) {
+        bulk_wait<D>();  // tile iter-D's stores are complete: its stage can be refilled
+        const uint32_t r = (iter - D) % D;
+        account(ring_item[r]);
+        const uint32_t nc = ring_chunk[r] + uint32_t(S);
+        if (nc < c_end) issue(nc, static_cast<int>((iter - D) % S));
       }
-      prev_item = this_item;
-      prev_chunk = chunk;
+      ring_item[iter % D] = this_item;
+      ring_chunk[iter % D] = chunk;
     }
   }
   if (tid == 0 && iter > 0) {
     bulk_wait<0>();
-    account(prev_item);
+    for (uint32_t j = iter > uint32_t(D) ? iter - D : 0; j < iter; ++j) account(ring_item[j % D]);
     flush();
   }
 }
@@ -528,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) optim_kernel(
 template <typename T, int KIND, bool UNDO, bool COPY_GRAD, bool PUSH = false>
 int launch_t(const LaunchArgs& a, cudaStream_t st) {
   auto kern = optim_kernel<T, KIND, UNDO, COPY_GRAD, PUSH>;
-  constexpr size_t smem = dyn_smem_bytes<T, KIND>();
+  constexpr size_t smem = dyn_smem_bytes<T, KIND, PUSH>();
   static int blocks_per_sm = -1;  // per instantiation (same on every B200)
   static int num_sms = -1;
   static unsigned long long dev_mask = 0;
