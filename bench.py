@@ -777,6 +777,54 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
                 gemm="tcgen05 kind::f16 M128xN256xK16, TMA SW128, TMEM double-buffered accumulators")
 
 
+def replay_subpipeline_bench(world: int, rank: int, device, iters: int = 2, rows: int = 16384, m: int = 8,
+                             dims=(4096, 16384, 4096), n_stages: int = 8) -> dict:
+    """Config 4, replay way (i): the 8-stage group folded onto the `world`
+    GPUs (contiguous blocks of stages, 1F1B, copy-engine boundaries); every
+    worker steps its own stages.  Same FLOPs as replay_bench."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import ADAM, OptimizerHyper
+    from paper_2302_06173_b200.replay import BoundaryLog, Stage, synth_inputs
+    from paper_2302_06173_b200.subpipeline import SubPipeline, recover_subpipeline, split_stages
+    h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
+    mine = list(split_stages(n_stages, world, rank))
+    sts = [Stage(s, dims[0], dims[1], dims[2], 2, 2302, ADAM, device=device.index) for s in mine]
+    log = BoundaryLog()
+    for mb in range(m):  # the group's inbound activations (worker 0) and gradients (last worker)
+        a = synth_inputs(5, 0, mb, rows, dims[0]) if rank == 0 else None
+        g = synth_inputs(6, 0, mb, rows, dims[-1]).mul_(1e-3) if rank == world - 1 else None
+        for it in range(iters + 1):
+            if a is not None:
+                log.acts[(it, mb)] = a
+            if g is not None:
+                log.grads[(it, mb)] = g
+    pipe = SubPipeline(sts, m, rows, dims[0])
+    layer = [2 * rows * dims[0] * dims[1], 2 * rows * dims[1] * dims[2]]
+    flop_it = m * (n_stages * 3 * sum(layer) - layer[0])
+    recover_subpipeline(pipe, log, 0, 1, 2302, h, first=False, last=False)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    recover_subpipeline(pipe, log, 1, 1 + iters, 2302, h, first=False, last=False)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / iters
+    del sts, log, pipe
+    torch.cuda.empty_cache()
+    sus = _peaks().get("bf16_sustained", 1382.3)
+    bubble = (world - 1) / (m + world - 1)
+    return dict(workload=f"config 4, replay way (i): {n_stages} stages folded onto {world} GPUs "
+                         f"({n_stages // world} per GPU), 1F1B over {m} micro-batches, copy-engine boundaries",
+                ms_per_iteration=round(ms, 3), tflops_aggregate=round(flop_it / (ms * 1e-3) / 1e12, 1),
+                frac_of_bf16_sustained_aggregate=round(flop_it / (ms * 1e-3) / 1e12 / (sus * world), 4),
+                pipeline_bubble=round(bubble, 4))
+
+
 def run_b200(args) -> None:
     import torch
     import torch.distributed as dist
@@ -877,6 +925,13 @@ def run_b200(args) -> None:
                     extras["replay"] = replay_bench(world, rank, device, iters=args.replay_iters)
                 except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
                     extras["replay"] = {"error": f"OOM: {e}"}
+                torch.cuda.empty_cache()
+                if world > 1:
+                    try:
+                        extras["replay_subpipeline"] = replay_subpipeline_bench(world, rank, device,
+                                                                                iters=args.replay_iters)
+                    except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
+                        extras["replay_subpipeline"] = {"error": f"OOM: {e}"}
     clocks = clk.summary()
     if rank != 0:
         if world > 1:

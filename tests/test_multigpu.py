@@ -34,10 +34,20 @@ def _run(fn, world=2):
     ps = [ctx.Process(target=_entry, args=(fn, r, world, port, q)) for r in range(world)]
     for p in ps:
         p.start()
-    out = dict(q.get(timeout=300) for _ in ps)
-    for p in ps:
-        p.join(timeout=120)
-        assert p.exitcode == 0
+    out = {}
+    try:
+        for _ in ps:
+            r, v = q.get(timeout=240)
+            out[r] = v
+            if isinstance(v, dict) and "error" in v:  # fail fast: a peer may be blocked on this rank
+                raise AssertionError(f"rank {r} raised:\n{v['error']}")
+    finally:
+        for p in ps:
+            p.join(timeout=60)
+            if p.exitcode is None:  # our own child, stuck behind a failed peer
+                p.kill()
+                p.join()
+    assert all(p.exitcode == 0 for p in ps)
     return out
 
 
@@ -48,6 +58,10 @@ def _entry(fn, rank, world, port, q):
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
         q.put((rank, fn(rank, world)))
+    except Exception:
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -206,3 +220,40 @@ def test_two_devices_in_one_process():
             sg.forward(acts)
             torch.cuda.synchronize(d)
     assert torch.equal(outs[0][0], outs[1][0]) and outs[0][1] == outs[1][1]
+
+
+def scen_subpipeline(rank, world):
+    """Replay way (i): the failed group's stages folded onto the 2 GPUs (1F1B,
+    copy-engine boundaries) == the ghost run bit for bit, for a middle group
+    and for a group ending at the loss."""
+    from paper_2302_06173_b200 import ADAM, OptimizerHyper
+    from paper_2302_06173_b200.replay import BoundaryLog, Pipeline, Stage
+    from paper_2302_06173_b200.subpipeline import SubPipeline, one_f_one_b, recover_subpipeline, split_stages
+    h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
+    res = {"sched": one_f_one_b(2, 4, rank)}
+    for name, grp, last in (("middle", (1, 3), False), ("tail", (1, 4), True)):
+        g = Pipeline(p=5, dim=64, hidden=96, layers=2, rows=96, micro_batches=4, seed=8, kind=ADAM, hyper=h)
+        log = BoundaryLog()
+        ids = list(range(grp[0], grp[1] + 1))
+        for it in range(3):
+            if it == 1:
+                snaps = {s: g.stages[s].snapshot() for s in ids}
+            g.run_iteration(log_group=grp, log=log)
+        mine = [ids[i] for i in split_stages(len(ids), world, rank)]
+        sts = [Stage(s, 64, 96, 64, 2, 8, ADAM) for s in mine]
+        for st, s in zip(sts, mine):
+            st.restore(snaps[s])
+        pipe = SubPipeline(sts, 4, 96, 64)
+        recover_subpipeline(pipe, log, 1, 3, 8, h, first=False, last=last)
+        res[name] = all(torch.equal(getattr(st.state, n), getattr(g.stages[s].state, n))
+                        for st, s in zip(sts, mine) for n in ("x", "m", "v"))
+    return res
+
+
+@needs2
+def test_subpipeline_replay_bitexact():
+    out = _run(scen_subpipeline)
+    assert out[0]["sched"] == [("F", 0), ("F", 1), ("B", 0), ("F", 2), ("B", 1), ("F", 3), ("B", 2), ("B", 3)]
+    assert out[1]["sched"] == [("F", 0), ("B", 0), ("F", 1), ("B", 1), ("F", 2), ("B", 2), ("F", 3), ("B", 3)]
+    for r in (0, 1):
+        assert out[r]["middle"] and out[r]["tail"], out[r]

@@ -16,8 +16,12 @@ torch.cuda.set_device(local)
 dev = torch.device("cuda", local)
 if world > 1:
     dist.init_process_group("nccl", device_id=dev)
-r = bench.replay_bench(world, rank, dev, iters=int(sys.argv[1]) if len(sys.argv) > 1 else 2)
+it = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+r = bench.replay_bench(world, rank, dev, iters=it)
+torch.cuda.empty_cache()
+r2 = bench.replay_subpipeline_bench(world, rank, dev, iters=it) if world > 1 else None
 if rank == 0:
-    print(json.dumps(r), flush=True)
+    print(json.dumps(dict(parallel=r["ms_per_iteration"], subpipeline=r2 and r2["ms_per_iteration"],
+                          bubble=r2 and r2["pipeline_bubble"])), flush=True)
 if world > 1:
     dist.destroy_process_group()
