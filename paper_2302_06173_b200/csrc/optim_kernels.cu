@@ -225,12 +225,21 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 
 constexpr int kThreads = 256;
-constexpr int kStages = 3;      // smem stages; 2 CTAs per SM
+#ifndef RW_OPTIM_STAGES
+#define RW_OPTIM_STAGES 3
+#endif
+#ifndef RW_OPTIM_SLOT_BYTES
+#define RW_OPTIM_SLOT_BYTES 8192
+#endif
+#ifndef RW_OPTIM_MIN_BLOCKS
+#define RW_OPTIM_MIN_BLOCKS 1
+#endif
+constexpr int kStages = RW_OPTIM_STAGES;  // smem stages (3 x 8 KB slots: 2 CTAs per SM)
 // fused NVLink push: 4 stages (2 tiles of stores in flight, 1 CTA per SM)
 // measured no faster than 3 (GPT-2 XL push 29.8 vs 29.9 ms), so 3
 constexpr int kStagesPush = 3;
-constexpr int kStagesMax = 4;
-constexpr uint32_t kSlotBytes = 8192;  // per stream per stage
+constexpr int kStagesMax = kStages > 4 ? kStages : 4;
+constexpr uint32_t kSlotBytes = RW_OPTIM_SLOT_BYTES;  // per stream per stage
 
 // per-stage tile descriptor, written by the producer thread before it arms
 // the stage's mbarrier (release) and read by all threads after the wait
@@ -262,7 +271,7 @@ constexpr size_t dyn_smem_bytes() {
 // from the same bulk-copy engine), and copy-only work items pass untouched
 // groups through to the peer: recover_replication fused with apply_undo.
 template <typename T, int KIND, bool UNDO, bool COPY_GRAD, bool PUSH>
-__global__ void __launch_bounds__(kThreads, 1) optim_kernel(
+__global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
     T* __restrict__ x, T* __restrict__ g, T* __restrict__ m, T* __restrict__ v,
     T* __restrict__ vmax, const T* __restrict__ grad, const WorkItem* __restrict__ work,
     uint32_t n_work, uint32_t total_chunks, const ScalarSet* __restrict__ sets, Uniform u,
