@@ -5,7 +5,7 @@
 set -e
 cd "$(dirname "$0")/.."
 ROOT=$(pwd)
-for v in "base:3:8192:1" "s4k4:4:4096:3" "s3k4:3:4096:3" "s6k4:6:4096:2"; do
+for v in ${VARIANTS:-"base:3:8192:1" "s4k4:4:4096:3" "s3k4:3:4096:3" "s6k4:6:4096:2"}; do
   IFS=: read name st sb mb <<< "$v"
   D=/tmp/optv/$name
   rm -rf $D; mkdir -p $D
@@ -15,7 +15,7 @@ for v in "base:3:8192:1" "s4k4:4:4096:3" "s3k4:3:4096:3" "s6k4:6:4096:2"; do
 done
 wait
 for round in 1 2; do
-for v in base s4k4 s3k4 s6k4; do
+for v in ${NAMES:-base s4k4 s3k4 s6k4}; do
   (cd /tmp && PYTHONPATH=/tmp/optv/$v:$ROOT python -) <<PY
 import sys, statistics, json
 import paper_2302_06173_b200 as P
