@@ -341,3 +341,34 @@ def test_full_size_configs_sampled_bitexact(restate, cfg):
     ux, um, uv, _ = restate.undo(ADAM, h, 21, rx, g0, rm, rv, dtype=np.float32)
     assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(ux))
     assert np.array_equal(_bits(st.v[idx].cpu().numpy()), _bits(uv))
+
+
+def test_group_beyond_2_pow_31_elements(restate):
+    """Maximum-size edge case: one group of 2^31 + 4099 fp32 elements (x, g, m,
+    v = 34 GB) plus a tiny trailing group — 64-bit offsets all the way through
+    the work list, the TMA tiles and the marker; sampled elements bit-exact,
+    both markers advanced."""
+    n_big = (1 << 31) + 4099
+    st = DeviceState([n_big, 33], kind=ADAM)
+    for i, k in enumerate(("x", "g", "m", "v")):
+        seeded_fill_(getattr(st, k), 60 + i)
+    st.m.mul_(0.01)
+    st.v.abs_().mul_(1e-4)
+    st.write_markers([(3, 0), (3, 0)])
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    idx = torch.cat([torch.randint(0, n_big, (1 << 18,), device="cuda", generator=gen),
+                     torch.arange(n_big - 64, n_big, device="cuda"),          # the tail of the big group
+                     torch.arange(st.offsets[1], st.offsets[1] + 33, device="cuda")])
+    x0, g0, m0, v0 = (getattr(st, k)[idx].cpu().numpy() for k in ("x", "g", "m", "v"))
+    h = HYP[ADAM]
+    st.step(h)
+    st.check_finite()
+    assert st.markers() == [(4, 1), (4, 1)]
+    rx, rm, rv, _ = restate.step(ADAM, h, 3, x0, g0, m0, v0, dtype=np.float32)
+    assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(rx))
+    assert np.array_equal(_bits(st.v[idx].cpu().numpy()), _bits(rv))
+    st.undo(h)
+    assert st.markers() == [(3, 0), (3, 0)]
+    ux, um, uv, _ = restate.undo(ADAM, h, 4, rx, g0, rm, rv, dtype=np.float32)
+    assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(ux))
+    assert np.array_equal(_bits(st.m[idx].cpu().numpy()), _bits(um))
