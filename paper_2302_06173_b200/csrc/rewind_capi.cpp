@@ -73,14 +73,19 @@ int lr_at(const rw_hyper* h, uint64_t t, double* out) {
 
 // Ring of per-launch metadata slots so back-to-back asynchronous calls never
 // overwrite a work list that a queued copy/kernel still reads.
+// The work list and the scalar sets of one launch sit back to back in one
+// pinned and one device buffer, so a launch uploads its metadata with one copy.
 struct Slot {
-  rwb::WorkItem* h_work = nullptr;  // pinned
-  rwb::ScalarSet* h_sets = nullptr; // pinned
+  uint8_t* h_buf = nullptr;  // pinned
+  uint8_t* d_buf = nullptr;
+  size_t buf_cap = 0;
+  rwb::WorkItem* h_work = nullptr;   // views into h_buf / d_buf for the current launch
+  rwb::ScalarSet* h_sets = nullptr;
   rwb::WorkItem* d_work = nullptr;
   rwb::ScalarSet* d_sets = nullptr;
+  size_t meta_bytes = 0;             // work + sets of the current launch
   uint32_t* d_done = nullptr;
   uint32_t cap = 0;
-  uint32_t set_cap = 0;
   cudaEvent_t ev = nullptr;
   bool used = false;
 };
@@ -126,27 +131,30 @@ int ensure_slot(rw_state* s, Slot& sl, uint32_t n_items, uint32_t n_sets) {
   if (sl.used) RW_CUDA(cudaEventSynchronize(sl.ev));
   if (!sl.ev) RW_CUDA(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
   if (n_items > sl.cap) {
-    cudaFreeHost(sl.h_work);
-    cudaFree(sl.d_work);
     cudaFree(sl.d_done);
-    sl.h_work = nullptr;
-    sl.d_work = nullptr;
     sl.d_done = nullptr;
     uint32_t cap = std::max<uint32_t>(n_items, 256);
-    RW_CUDA(cudaMallocHost(&sl.h_work, sizeof(rwb::WorkItem) * cap));
-    RW_CUDA(cudaMalloc(&sl.d_work, sizeof(rwb::WorkItem) * cap));
     RW_CUDA(cudaMalloc(&sl.d_done, sizeof(uint32_t) * cap));
     RW_CUDA(cudaMemset(sl.d_done, 0, sizeof(uint32_t) * cap));
     sl.cap = cap;
   }
-  if (n_sets > sl.set_cap) {
-    cudaFreeHost(sl.h_sets);
-    cudaFree(sl.d_sets);
-    uint32_t cap = std::max<uint32_t>(n_sets, 16);
-    RW_CUDA(cudaMallocHost(&sl.h_sets, sizeof(rwb::ScalarSet) * cap));
-    RW_CUDA(cudaMalloc(&sl.d_sets, sizeof(rwb::ScalarSet) * cap));
-    sl.set_cap = cap;
+  static_assert(sizeof(rwb::WorkItem) % alignof(rwb::ScalarSet) == 0, "sets follow the work items");
+  const size_t need = sizeof(rwb::WorkItem) * n_items + sizeof(rwb::ScalarSet) * n_sets;
+  if (need > sl.buf_cap) {
+    cudaFreeHost(sl.h_buf);
+    cudaFree(sl.d_buf);
+    sl.h_buf = nullptr;
+    sl.d_buf = nullptr;
+    const size_t cap = std::max<size_t>(need, 16384);
+    RW_CUDA(cudaMallocHost(&sl.h_buf, cap));
+    RW_CUDA(cudaMalloc(&sl.d_buf, cap));
+    sl.buf_cap = cap;
   }
+  sl.h_work = reinterpret_cast<rwb::WorkItem*>(sl.h_buf);
+  sl.d_work = reinterpret_cast<rwb::WorkItem*>(sl.d_buf);
+  sl.h_sets = reinterpret_cast<rwb::ScalarSet*>(sl.h_buf + sizeof(rwb::WorkItem) * n_items);
+  sl.d_sets = reinterpret_cast<rwb::ScalarSet*>(sl.d_buf + sizeof(rwb::WorkItem) * n_items);
+  sl.meta_bytes = need;
   (void)s;
   return RW_OK;
 }
@@ -224,10 +232,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
   if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one call");
   auto cs = static_cast<cudaStream_t>(stream);
   if (n_items > 0) {
-    RW_CUDA(cudaMemcpyAsync(sl.d_work, sl.h_work, sizeof(rwb::WorkItem) * n_items,
-                            cudaMemcpyHostToDevice, cs));
-    RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * n_sets,
-                            cudaMemcpyHostToDevice, cs));
+    RW_CUDA(cudaMemcpyAsync(sl.d_buf, sl.h_buf, sl.meta_bytes, cudaMemcpyHostToDevice, cs));  // work + sets
     if (lamb && !undo) {
       // step_lamb first pass over every group: m, v, both norms, trust
       if (s->partial_cap < chunk) {
@@ -430,10 +435,8 @@ void rw_state_destroy(rw_state* s) {
       cudaEventSynchronize(sl.ev);
       cudaEventDestroy(sl.ev);
     }
-    cudaFreeHost(sl.h_work);
-    cudaFreeHost(sl.h_sets);
-    cudaFree(sl.d_work);
-    cudaFree(sl.d_sets);
+    cudaFreeHost(sl.h_buf);
+    cudaFree(sl.d_buf);
     cudaFree(sl.d_done);
   }
   cudaFree(s->d_groups);
@@ -757,8 +760,7 @@ int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, 
     if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one slice");
     chunks[k] = static_cast<uint32_t>(chunk);
   }
-  RW_CUDA(cudaMemcpyAsync(sl.d_work, sl.h_work, sizeof(rwb::WorkItem) * n, cudaMemcpyHostToDevice, cs));
-  RW_CUDA(cudaMemcpyAsync(sl.d_sets, sl.h_sets, sizeof(rwb::ScalarSet) * n_sets, cudaMemcpyHostToDevice, cs));
+  RW_CUDA(cudaMemcpyAsync(sl.d_buf, sl.h_buf, sl.meta_bytes, cudaMemcpyHostToDevice, cs));  // work + sets
   const size_t es = elem_size(s->dtype);
   cudaEvent_t start = s->evs[3 * slices.size()];
   RW_CUDA(cudaEventRecord(start, cs));  // prior work + the metadata upload first
