@@ -187,10 +187,14 @@ def scen_parallel_replay(rank, world):
     return res
 
 
+WORLD = min(4, torch.cuda.device_count()) if torch.cuda.is_available() else 0
+
+
 @needs2
-def test_parallel_replay_two_ranks_bitexact():
-    out = _run(scen_parallel_replay)
-    for r in (0, 1):
+def test_parallel_replay_bitexact():
+    """All visible GPUs (up to 4) as helpers."""
+    out = _run(scen_parallel_replay, world=WORLD)
+    for r in range(WORLD):
         assert out[r]["eq_seq"] and out[r]["eq_ghost"]
         assert out[r]["eq_group"]
 
@@ -223,7 +227,7 @@ def test_two_devices_in_one_process():
 
 
 def scen_subpipeline(rank, world):
-    """Replay way (i): the failed group's stages folded onto the 2 GPUs (1F1B,
+    """Replay way (i): the failed group's stages folded onto the GPUs (1F1B,
     copy-engine boundaries) == the ghost run bit for bit, for a middle group
     and for a group ending at the loss."""
     from paper_2302_06173_b200 import ADAM, OptimizerHyper
@@ -231,8 +235,9 @@ def scen_subpipeline(rank, world):
     from paper_2302_06173_b200.subpipeline import SubPipeline, one_f_one_b, recover_subpipeline, split_stages
     h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
     res = {"sched": one_f_one_b(2, 4, rank)}
-    for name, grp, last in (("middle", (1, 3), False), ("tail", (1, 4), True)):
-        g = Pipeline(p=5, dim=64, hidden=96, layers=2, rows=96, micro_batches=4, seed=8, kind=ADAM, hyper=h)
+    # 4-stage groups of a 7-stage pipeline: 2 stages per GPU at d=2, 1 at d=4
+    for name, grp, last in (("middle", (1, 4), False), ("tail", (3, 6), True)):
+        g = Pipeline(p=7, dim=64, hidden=96, layers=2, rows=96, micro_batches=4, seed=8, kind=ADAM, hyper=h)
         log = BoundaryLog()
         ids = list(range(grp[0], grp[1] + 1))
         for it in range(3):
@@ -252,8 +257,9 @@ def scen_subpipeline(rank, world):
 
 @needs2
 def test_subpipeline_replay_bitexact():
-    out = _run(scen_subpipeline)
+    """All visible GPUs (up to 4) as pipeline workers."""
+    out = _run(scen_subpipeline, world=WORLD)
     assert out[0]["sched"] == [("F", 0), ("F", 1), ("B", 0), ("F", 2), ("B", 1), ("F", 3), ("B", 2), ("B", 3)]
     assert out[1]["sched"] == [("F", 0), ("B", 0), ("F", 1), ("B", 1), ("F", 2), ("B", 2), ("F", 3), ("B", 3)]
-    for r in (0, 1):
+    for r in range(WORLD):
         assert out[r]["middle"] and out[r]["tail"], out[r]
