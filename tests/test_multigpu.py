@@ -263,3 +263,43 @@ def test_subpipeline_replay_bitexact():
     assert out[1]["sched"] == [("F", 0), ("B", 0), ("F", 1), ("B", 1), ("F", 2), ("B", 2), ("F", 3), ("B", 3)]
     for r in range(WORLD):
         assert out[r]["middle"] and out[r]["tail"], out[r]
+
+
+def scen_recovery_all(rank, world):
+    """Replica recovery to every other rank (1 survivor, world-1 replacements):
+    pipelined (undo overlapped with per-buffer NCCL broadcasts) and
+    undo-then-broadcast give every rank the survivor's resolved bits."""
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import ADAM, DeviceState, OptimizerHyper, seeded_fill_
+    from paper_2302_06173_b200.logstore import crc32_device
+    from paper_2302_06173_b200.recovery import recover, resolve
+    sizes = [100_003, 64, 2_000_017, 7, 1_234_567, 4096, 77]
+    h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
+    out = {}
+    for transfer in ("pipelined", "broadcast"):
+        st = DeviceState(sizes, kind=ADAM)
+        if rank == 0:
+            for i, t in enumerate((st.x, st.g, st.m, st.v)):
+                seeded_fill_(t, 50 + i)
+            st.v.abs_()
+            st.write_markers([(9, 0)] * len(sizes))
+            st.step(h, stop_after=4)
+        plan = resolve(st.markers() if rank == 0 else [], h, lens=sizes if rank == 0 else None)
+        used, _ = recover(st, h, plan, src=0, transfer=transfer)
+        crc = [crc32_device(torch.cat([st.view(n, i) for i in range(len(sizes))]).view(torch.uint8))
+               for n in ("x", "m", "v")]
+        allc = [None] * world
+        dist.all_gather_object(allc, (crc, st.markers()))
+        out[transfer] = dict(used=used, same=all(c == allc[0] for c in allc), strategy=plan.strategy,
+                             markers=st.markers())
+    return out
+
+
+@needs2
+def test_recovery_to_all_ranks_bitexact():
+    out = _run(scen_recovery_all, world=WORLD)
+    for r in range(WORLD):
+        for tr in ("pipelined", "broadcast"):
+            assert out[r][tr]["same"] and out[r][tr]["strategy"] == "Undo", (r, tr, out[r][tr])
+            assert out[r][tr]["markers"] == [(9, 0)] * 7
