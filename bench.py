@@ -635,6 +635,9 @@ def checkpoint_bench(sizes, reps: int = 2) -> dict:
         torch.cuda.empty_cache()
 
 
+RECOVERY_MODES = None  # override for experiments (tools/recovery_scale.py)
+
+
 def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     """Config 3: replica recovery of a GPT-2 XL Adam state.  Rank 0 is the
     survivor, crashed mid-update after half the groups (MidUpdate(G/2));
@@ -657,7 +660,8 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     if rank == 0:
         _fill_adam_state(st)
     out = {}
-    modes = ["nccl", "pipelined", "scatter_allgather", "fused", "auto"] if world > 1 else ["local"]
+    modes = (RECOVERY_MODES or ["nccl", "pipelined", "chain", "scatter_allgather", "fused", "auto"]) if world > 1 \
+        else ["local"]
     for mode in modes:
         res = []
         kinfo = []
@@ -672,7 +676,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
             plan = resolve(st.markers() if rank == 0 else [], h, lens=sizes if rank == 0 else None,
                            device=device)
             t_resolved = time.perf_counter()
-            if mode in ("auto", "scatter_allgather", "pipelined"):
+            if mode in ("auto", "scatter_allgather", "pipelined", "chain"):
                 used, nbytes = recover(st, h, plan, src=0, transfer=mode)
                 kinfo.append({"used": used})
             elif mode == "fused":

@@ -375,24 +375,141 @@ def recover_replication_pipelined(state, hyper, plan: ResolvePlan, src: int, inc
     return sum(sum(state.sizes) * getattr(state, n).element_size() for n in names)
 
 
+_CE_CHAINS: dict = {}
+
+
+def _runs_of(state, pieces: int) -> list[tuple[int, int]]:
+    """Contiguous runs of groups of ~total/pieces elements (same on every rank)."""
+    G, total = state.num_groups, sum(state.sizes)
+    runs, start, acc = [], 0, 0
+    for i, n in enumerate(state.sizes):
+        acc += n
+        if acc >= total * (len(runs) + 1) / pieces or i == G - 1:
+            runs.append((start, i + 1))
+            start = i + 1
+    return runs
+
+
+def recover_replication_chain(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False,
+                              group=None, pieces: int = 16, split: int = 1) -> int:
+    """apply_undo + recover_replication over the copy engines, as a pipelined
+    chain: the survivor undoes run i of the groups while its DMA engines push
+    the already-resolved run i-1 into the first replacement's HBM (CUDA IPC);
+    each replacement forwards every run to the next one as soon as the run's
+    epoch counter lands (cuStreamWaitValue64 -> cudaMemcpyAsync ->
+    cuStreamWriteValue64, all stream-ordered, no kernel).  The copy engines
+    write NVLink at ~780 GB/s against ~717 for SM stores (tools/peer_bw.cu),
+    every link carries the state once, and the chain adds only one run's
+    transfer per extra hop.  Returns bytes per replacement."""
+    if not (dist.is_available() and dist.is_initialized()):
+        raise RwError(17, "NoReplica: no process group")
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    names = ["x"] + (["g"] if include_grad else []) + [n for n in ("m", "v") if getattr(state, n) is not None]
+    runs = _runs_of(state, pieces)  # undo granularity (whole groups)
+    # copy granularity: every run's element span in `split` equal sub-ranges
+    # (copies need no group alignment), so each hop lags one sub-range only
+    spans = []
+    for g0, g1 in runs:
+        lo, hi = state.offsets[g0], state.offsets[g1 - 1] + state.sizes[g1 - 1]
+        step = -(-(hi - lo) // split)
+        spans.append([(a, min(hi, a + step)) for a in range(lo, hi, step)])
+    n_pieces = sum(len(sp) for sp in spans)
+    # handles are exchanged on every call (the peers' buffers may have moved);
+    # the mappings themselves are cached by handle in _PEER_MAPS
+    counters = torch.zeros(n_pieces, dtype=torch.int64, device=state.device)
+    mine = dict(bufs={n: _export(getattr(state, n)) for n in names}, counters=_export(counters))
+    allh: list = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    chain = [src] + [r for r in range(world) if r != src]
+    pos = chain.index(rank)
+    nxt = None
+    if pos + 1 < world:
+        h = allh[chain[pos + 1]]
+
+        def mapped(hh):
+            hb, off = hh
+            if hb not in _PEER_MAPS:
+                base = C.c_void_p()
+                check(LIB.rw_ipc_import(hb, C.byref(base)))
+                _PEER_MAPS[hb] = base
+            return _PEER_MAPS[hb].value + off
+
+        nxt = dict(bufs={n: mapped(h["bufs"][n]) for n in names}, counters=mapped(h["counters"]))
+    dkey = state.device.index
+    if dkey not in _CE_CHAINS:
+        _CE_CHAINS[dkey] = torch.cuda.Stream(device=state.device)
+    cs, ep = _CE_CHAINS[dkey], 1
+    sh = C.c_void_p(cs.cuda_stream)
+    undo = set(plan.undo_ids) if plan.strategy == STRATEGY_NAMES[STRATEGY_UNDO] else set()
+    if rank == src and plan.strategy not in (STRATEGY_NAMES[STRATEGY_UNDO], "None"):
+        apply_resolution(state, hyper, plan)
+    if rank == src and undo:
+        mk = state.markers()
+        if any(mk[i][1] == 0 for i in undo):
+            state.write_markers([(t, 1 if i in undo else u) for i, (t, u) in enumerate(mk)])
+    es = getattr(state, names[0]).element_size()
+    cptr = counters.data_ptr()
+    piece = 0
+    for (g0, g1), span in zip(runs, spans):
+        if rank == src:
+            ids = [j for j in range(g0, g1) if j in undo]
+            if ids:
+                state.undo(hyper, ids)
+            ev = torch.cuda.Event()
+            ev.record()
+            cs.wait_event(ev)
+        for lo, hi in span:
+            if rank != src:  # wait until the previous hop's copy of this piece has landed
+                check(LIB.rw_stream_wait_u64(sh, C.c_void_p(cptr + 8 * piece), ep))
+            if nxt is not None:
+                n = len(names)
+                dsts = (C.c_void_p * n)(*[nxt["bufs"][nm] + lo * es for nm in names])
+                srcs = (C.c_void_p * n)(*[getattr(state, nm).data_ptr() + lo * es for nm in names])
+                nbytes = (C.c_uint64 * n)(*[(hi - lo) * es] * n)
+                check(LIB.rw_copy_async(dsts, srcs, nbytes, n, sh))
+                check(LIB.rw_stream_write_u64(sh, C.c_void_p(nxt["counters"] + 8 * piece), ep))
+            piece += 1
+    torch.cuda.current_stream().wait_stream(cs)
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)  # every hop has landed everywhere (counters may now be freed)
+    _broadcast_saved_scalars(state, src, group)
+    mk = state.markers()
+    backend = dist.get_backend(group)
+    dev = state.device if backend == "nccl" else torch.device("cpu")
+    t = torch.tensor([v for pair in mk for v in pair], dtype=torch.int64, device=dev)
+    dist.broadcast(t, src=src, group=group)
+    flat = t.cpu().tolist()
+    state.write_markers([(flat[2 * i], flat[2 * i + 1]) for i in range(len(mk))])
+    return sum(sum(state.sizes) * getattr(state, n).element_size() for n in names)
+
+
 def recover(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False, group=None,
             transfer: str = "auto") -> tuple[str, int]:
     """apply_undo + recover_replication (SPEC:484-501).  transfer:
-      "pipelined" (auto): the undo run by run overlapped with concurrent async
-          NCCL broadcasts of the resolved runs (one communicator per buffer);
+      "chain": the undo run by run overlapped with copy-engine pushes of the
+          resolved runs into the next rank's HBM (CUDA IPC), each replacement
+          forwarding to the next (auto for one replacement);
+      "pipelined": the undo run by run overlapped with concurrent async NCCL
+          broadcasts of the resolved runs, one communicator per buffer (auto
+          for several replacements);
       "fused": one kernel undoes and pushes every tile into the replacement's
-          HBM over NVLink (CUDA IPC; one replacement at a time);
+          HBM with SM bulk stores (one replacement at a time);
       "broadcast": undo, then ncclBroadcast; "scatter_allgather".
-    Measured for GPT-2 XL (18.7 GB): N=2 pipelined 28.2 ms, fused 29.9,
-    broadcast 31.5; N=4 pipelined 28.7, broadcast 32.0, scatter+all-gather
-    46.1, fused (sequential pushes) 82.1.  Returns (transfer used, bytes per
-    replacement)."""
-    if transfer == "auto":
-        transfer = "pipelined"
+    Measured for GPT-2 XL (18.7 GB, resolve included): N=2 chain 26.6-26.7 ms,
+    pipelined 27.9, fused 29.5-29.9, broadcast 31.0-31.5; N=4 pipelined
+    28.4-28.8, chain 29.1-30.1 (one sub-range of lag per hop), broadcast 32.0-32.4,
+    scatter+all-gather 45.8-46.1, fused (sequential pushes) 82.  NVLink write
+    bandwidth by engine (tools/peer_bw.cu): copy engines 781 GB/s, SM stores
+    (TMA bulk or st.v4) 717.  Returns (transfer used, bytes per replacement)."""
+    if transfer == "auto":  # measured best per replacement count (see the docstring)
+        world = dist.get_world_size(group)
+        transfer = "chain" if (world == 2 and world <= torch.cuda.device_count()) else "pipelined"
     if transfer == "fused":
         return transfer, recover_replication_fused(state, hyper, plan, src, include_grad, group)
     if transfer == "pipelined":
         return transfer, recover_replication_pipelined(state, hyper, plan, src, include_grad, group)
+    if transfer == "chain":
+        return transfer, recover_replication_chain(state, hyper, plan, src, include_grad, group)
     if dist.get_rank(group) == src:
         apply_resolution(state, hyper, plan)
     algo = "scatter_allgather" if transfer == "scatter_allgather" else "broadcast"

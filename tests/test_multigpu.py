@@ -277,7 +277,7 @@ def scen_recovery_all(rank, world):
     sizes = [100_003, 64, 2_000_017, 7, 1_234_567, 4096, 77]
     h = OptimizerHyper(kind=ADAM, lr=1e-3, weight_decay=0.01)
     out = {}
-    for transfer in ("pipelined", "broadcast"):
+    for transfer in ("pipelined", "broadcast", "chain"):
         st = DeviceState(sizes, kind=ADAM)
         if rank == 0:
             for i, t in enumerate((st.x, st.g, st.m, st.v)):
@@ -300,6 +300,6 @@ def scen_recovery_all(rank, world):
 def test_recovery_to_all_ranks_bitexact():
     out = _run(scen_recovery_all, world=WORLD)
     for r in range(WORLD):
-        for tr in ("pipelined", "broadcast"):
+        for tr in ("pipelined", "broadcast", "chain"):
             assert out[r][tr]["same"] and out[r][tr]["strategy"] == "Undo", (r, tr, out[r][tr])
             assert out[r][tr]["markers"] == [(9, 0)] * 7

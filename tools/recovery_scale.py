@@ -8,6 +8,15 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import bench  # noqa: E402
+from paper_2302_06173_b200 import recovery as _rec  # noqa: E402
+
+if os.environ.get("RW_CHAIN"):  # sweep hook: "pieces,split" of the copy-engine chain
+    _p, _s = (int(v) for v in os.environ["RW_CHAIN"].split(","))
+    _d = list(_rec.recover_replication_chain.__defaults__)
+    _d[-2], _d[-1] = _p, _s
+    _rec.recover_replication_chain.__defaults__ = tuple(_d)
+if os.environ.get("RW_MODES"):
+    bench.RECOVERY_MODES = os.environ["RW_MODES"].split(",")
 
 rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(
     os.environ.get("LOCAL_RANK", 0))
