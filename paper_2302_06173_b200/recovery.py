@@ -315,12 +315,26 @@ def _buffer_comms(k: int, group=None) -> list:
 
 def prepare_transfer(state, include_grad: bool = False, group=None) -> None:
     """Create and connect the per-buffer communicators of the pipelined
-    transfer ahead of time (collective): right after a repaired process group
-    is formed, so the recovery itself does not pay NCCL initialisation."""
+    transfer and map every peer's state buffers for the copy-engine chain,
+    ahead of time (collective): right after a repaired process group is
+    formed, so the recovery itself pays neither NCCL initialisation nor CUDA
+    IPC mapping."""
     names = ["x"] + (["g"] if include_grad else []) + [n for n in ("m", "v") if getattr(state, n) is not None]
     for cg in _buffer_comms(len(names), group):
         dev = state.device if dist.get_backend(cg) == "nccl" else torch.device("cpu")
         dist.all_reduce(torch.zeros(1, device=dev), group=cg)
+    if dist.get_backend(group) == "nccl":  # and map every peer's buffers for the copy-engine chain
+        mine = {n: _export(getattr(state, n)) for n in names}
+        allh: list = [None] * dist.get_world_size(group)
+        dist.all_gather_object(allh, mine, group=group)
+        for r, h in enumerate(allh):
+            if r == dist.get_rank(group):
+                continue
+            for hb, _ in h.values():
+                if hb not in _PEER_MAPS:
+                    base = C.c_void_p()
+                    check(LIB.rw_ipc_import(hb, C.byref(base)))
+                    _PEER_MAPS[hb] = base
 
 
 def recover_replication_pipelined(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False,
