@@ -303,3 +303,48 @@ def test_recovery_to_all_ranks_bitexact():
         for tr in ("pipelined", "broadcast", "chain"):
             assert out[r][tr]["same"] and out[r][tr]["strategy"] == "Undo", (r, tr, out[r][tr])
             assert out[r][tr]["markers"] == [(9, 0)] * 7
+
+
+def scen_lamb_recovery(rank, world):
+    """LAMB (saved trust ratios) through the chain and pipelined transfers:
+    the replacement gets the survivor's state AND its trust-ratio stacks, so a
+    later undo on the replacement matches the survivor's bit for bit."""
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200 import LAMB, DeviceState, OptimizerHyper, seeded_fill_
+    from paper_2302_06173_b200.recovery import recover, resolve
+    sizes = [50_001, 4096, 777, 300_000]
+    h = OptimizerHyper(kind=LAMB, lr=1e-3, weight_decay=0.01)
+    out = {}
+    for transfer in ("chain", "pipelined"):
+        st = DeviceState(sizes, kind=LAMB)
+        if rank == 0:
+            for i, t in enumerate((st.x, st.g, st.m, st.v)):
+                seeded_fill_(t, 70 + i)
+            st.v.abs_()
+            st.write_markers([(4, 0)] * len(sizes))
+            st.step(h)                 # a completed LAMB step (ratios saved) ...
+            st.clear_updated()
+            st.step(h, stop_after=2)   # ... then a torn one
+        plan = resolve(st.markers() if rank == 0 else [], h, lens=sizes if rank == 0 else None)
+        recover(st, h, plan, src=0, transfer=transfer)
+        # everyone undoes the completed step with its (replicated) saved ratio
+        st.write_markers([(5, 1)] * len(sizes))
+        st.undo(h)
+        x = st.x.clone()
+        allx = [torch.empty_like(x) for _ in range(world)]
+        dist.all_gather(allx, x)
+        out[transfer] = dict(strategy=plan.strategy,
+                             same=all(torch.equal(a[o:o + n], allx[0][o:o + n]) for a in allx
+                                      for o, n in zip(st.offsets, st.sizes)),
+                             saved=[len(st.saved_scalars(i)) for i in range(len(sizes))])
+    return out
+
+
+@needs2
+def test_lamb_recovery_replicates_saved_ratios():
+    out = _run(scen_lamb_recovery, world=WORLD)
+    for r in range(WORLD):
+        for tr in ("chain", "pipelined"):
+            assert out[r][tr]["strategy"] == "Undo" and out[r][tr]["same"], (r, tr, out[r][tr])
+            assert out[r][tr]["saved"] == [0, 0, 0, 0]
