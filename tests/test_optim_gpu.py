@@ -274,23 +274,32 @@ def test_large_state_roundtrip_sampled(restate):
     assert ((st.x - x0).abs() <= 2 * torch.finfo(torch.float32).eps * sp + 1e-30).all()
 
 
-@pytest.mark.parametrize("kind", [ADAM, SGDM])
-def test_undo_from_host_pipelined_equals_device_undo(kind):
+@pytest.mark.parametrize("kind,dtype", [(ADAM, torch.float32), (SGDM, torch.float32), (ADAM, torch.float64),
+                                         ("lamb", torch.float32)])
+def test_undo_from_host_pipelined_equals_device_undo(kind, dtype):
     """rw_optimizer_undo_host (H2D | undo | D2H pipelined per slice) gives the
-    same bits and markers as the device-resident undo, for many small slices."""
+    same bits and markers as the device-resident undo, for many small slices;
+    LAMB's host-resident undo takes the saved trust ratios of the staging state."""
+    from paper_2302_06173_b200 import LAMB
+    lamb = kind == "lamb"
+    kind = LAMB if lamb else kind
+    h = OptimizerHyper(kind=LAMB, lr=1e-3, weight_decay=0.01) if lamb else HYP[kind]
     sizes = [1000, 77, 5000, 64, 3000, 12345]
-    h = HYP[kind]
-    ref = DeviceState(sizes, dtype=torch.float32, kind=kind)
+    ref = DeviceState(sizes, dtype=dtype, kind=kind)
     seeded_fill_(ref.x, 1)
     seeded_fill_(ref.g, 2)
     seeded_fill_(ref.m, 3)
     if ref.v is not None:
         seeded_fill_(ref.v, 4)
         ref.v.abs_()
-    ref.write_markers([(5, 1)] * len(sizes))
+    ref.write_markers([(5, 0)] * len(sizes))
+    ref.step(h)  # the pending update to undo (LAMB saves its trust ratios here)
     host = {k: getattr(ref, k).cpu().pin_memory() for k in ("x", "g", "m", "v") if getattr(ref, k) is not None}
-    st = DeviceState(sizes, dtype=torch.float32, kind=kind)
-    st.write_markers([(5, 1)] * len(sizes))
+    st = DeviceState(sizes, dtype=dtype, kind=kind)
+    st.write_markers(ref.markers())
+    if lamb:
+        for i in range(len(sizes)):
+            st.set_saved_scalars(i, ref.saved_scalars(i))
     out = {k: torch.zeros_like(v).pin_memory() for k, v in host.items() if k != "g"}
     ids = [5, 3, 1, 0]
     st.undo_from_host(h, host, out, ids=ids, slice_elems=2000)
@@ -302,6 +311,8 @@ def test_undo_from_host_pipelined_equals_device_undo(kind):
         assert torch.equal(out[k][lo:hi].cuda(), getattr(ref, k)[lo:hi]), k
         assert torch.equal(getattr(st, k)[lo:hi], getattr(ref, k)[lo:hi]), k
     assert st.markers() == ref.markers()
+    if lamb:
+        assert [len(st.saved_scalars(i)) for i in ids] == [0] * len(ids)
     with pytest.raises(RwError) as e:  # guards before any copy
         st.undo_from_host(h, host, out, ids=[0])
     assert e.value.name == "NothingToUndo"
