@@ -34,9 +34,12 @@ def _close(gpu, ref, tol=TOL):
     return err <= tol * scale + 1e-6, (err, scale)
 
 
-def test_stage_forward_backward_vs_reference(ref):
+@pytest.mark.parametrize("din,dh,dout,rows", [(64, 128, 64, 256),     # the desk shape
+                                              (256, 1024, 256, 256),   # 4x expansion, K = 1024 accumulations
+                                              (96, 200, 56, 100)])     # ragged: no dimension a tile multiple
+def test_stage_forward_backward_vs_reference(ref, din, dh, dout, rows):
     torch.manual_seed(0)
-    sid, din, dh, dout, L, seed, rows = 1, 64, 128, 64, 2, 2302, 256
+    sid, L, seed = 1, 2, 2302
     st = Stage(sid, din, dh, dout, L, seed, ADAM)
     rs = ref.L.ref_stage_make(sid, din, dh, dout, L, seed)
     assert rs
