@@ -718,7 +718,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
 
 
 def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 16384, m: int = 8,
-                 dims=(4096, 16384, 4096), n_stages: int = 8) -> dict:
+                 dims=(4096, 16384, 4096), n_stages: int = 8, pinned_logs: bool = False) -> dict:
     """Config 4: logging-based replay of the failed machine's 8-stage group
     (each stage two affine+tanh layers 4096 -> 16384 -> 4096),
     micro-batch 8 x 2048 tokens = 16384 rows, m = 8 micro-batches, Adam, from
@@ -733,11 +733,13 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
     from paper_2302_06173_b200.replay import BoundaryLog, Stage, recover_parallel, replay_group, synth_inputs
     h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
     sts = [Stage(s, dims[0], dims[1], dims[2], 2, 2302, ADAM, device=device.index) for s in range(n_stages)]
-    log = BoundaryLog()
+    log = BoundaryLog(pinned=pinned_logs)
     mine = [mb for mb in range(m) if mb % world == rank]
     for mb in mine:  # synthetic logged tensors for this helper's micro-batches
         a = synth_inputs(5, 0, mb, rows, dims[0])
         g = synth_inputs(6, 0, mb, rows, dims[-1]).mul_(1e-3)
+        if pinned_logs:  # logs held in pinned host memory (north_star): H2D inside the timed region
+            a, g = a.cpu().pin_memory(), g.cpu().pin_memory()
         for it in range(iters + 1):
             log.acts[(it, mb)] = a
             log.grads[(it, mb)] = g
@@ -770,9 +772,10 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
     del sts, log
     torch.cuda.empty_cache()
     sus = _peaks().get("bf16_sustained", 1382.3)
+    where = "pinned host memory (prefetched H2D)" if pinned_logs else "HBM"
     return dict(workload=f"config 4: replay of the failed {n_stages}-stage group (each stage 4096->16384->4096 "
                          f"affine+tanh, Adam; {n_stages * 134}M params), {m} micro-batches x {rows} rows, logs in "
-                         f"HBM, parallel recovery over {world} GPU(s)",
+                         f"{where}, parallel recovery over {world} GPU(s)",
                 iterations=iters, ms_per_iteration=round(ms_max / iters, 3),
                 tflops_aggregate=round(tflops, 1), tflop_per_iteration=round(flop_it / 1e12, 2),
                 roofline_ms_per_iteration=round(flop_it / (sus * world * 1e12) * 1e3, 2),
@@ -930,6 +933,13 @@ def run_b200(args) -> None:
                 except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
                     extras["replay"] = {"error": f"OOM: {e}"}
                 torch.cuda.empty_cache()
+                if world == 1:
+                    try:
+                        extras["replay_pinned_logs"] = replay_bench(world, rank, device, iters=args.replay_iters,
+                                                                    pinned_logs=True)
+                    except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
+                        extras["replay_pinned_logs"] = {"error": f"OOM: {e}"}
+                    torch.cuda.empty_cache()
                 if world > 1:
                     try:
                         extras["replay_subpipeline"] = replay_subpipeline_bench(world, rank, device,

@@ -221,6 +221,8 @@ class BoundaryLog:
     acts: dict = field(default_factory=dict)    # (it, mb) -> tensor
     grads: dict = field(default_factory=dict)
     pinned: bool = False
+    _pending: dict = field(default_factory=dict, repr=False)  # prefetched H2D copies
+    _stream: object = field(default=None, repr=False)
 
     def put(self, kind: str, it: int, mb: int, t: torch.Tensor, sender: int = 0, receiver: int = 0) -> None:
         if self.pinned:
@@ -231,7 +233,30 @@ class BoundaryLog:
             t = t.clone()
         (self.acts if kind == "act" else self.grads)[(it, mb)] = t
 
+    def prefetch(self, kind: str, it: int, mb: int, device) -> None:
+        """Start the H2D copy of a host-resident record on a side stream, so it
+        overlaps the replay compute (get() then only waits for it)."""
+        if not self.pinned:
+            return
+        t = (self.acts if kind == "act" else self.grads).get((it, mb))
+        key = (kind, it, mb)
+        if t is None or t.device == device or key in self._pending:
+            return
+        if self._stream is None:
+            self._stream = torch.cuda.Stream(device=device)
+        with torch.cuda.stream(self._stream):
+            dev_t = t.to(device, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(self._stream)
+        self._pending[key] = (dev_t, ev)
+
     def get(self, kind: str, it: int, mb: int, device) -> torch.Tensor | None:
+        hit = self._pending.pop((kind, it, mb), None)
+        if hit is not None:  # prefetched: wait for its copy, keep the memory alive for this stream
+            dev_t, ev = hit
+            torch.cuda.current_stream().wait_event(ev)
+            dev_t.record_stream(torch.cuda.current_stream())
+            return dev_t
         d = self.acts if kind == "act" else self.grads
         t = d.get((it, mb))
         if t is None:
@@ -313,6 +338,14 @@ def replay_group(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, 
     dev = stages[0].device
     for it in range(it0, it1):
         for mb in range(micro_batches):
+            # host-resident logs: this micro-batch's gradient and the next one's
+            # activation move while this micro-batch computes
+            if not last:
+                log.prefetch("grad", it, mb, dev)
+            if not first:
+                nxt = (it, mb + 1) if mb + 1 < micro_batches else (it + 1, 0)
+                log.prefetch("act", it, mb, dev)
+                log.prefetch("act", nxt[0], nxt[1], dev)
             if first:
                 x = synth_inputs(seed, it, mb, rows, dim, device=dev)
             else:
@@ -340,6 +373,7 @@ def replay_group(stages: Sequence[Stage], log: BoundaryLog, it0: int, it1: int, 
                 g = gout
         for st in reversed(stages):
             st.step(hyper)
+    log._pending.clear()  # a prefetch past the replayed range is not needed
     return it1 - it0
 
 
@@ -359,6 +393,12 @@ def helper_pass(stages: Sequence[Stage], log: BoundaryLog, it: int, mbs: Sequenc
     dev = stages[0].device
     out = {}
     for n_mb, mb in enumerate(mbs):
+        if not last:  # host-resident logs: overlap their H2D with this helper's compute
+            log.prefetch("grad", it, mb, dev)
+        if not first:
+            log.prefetch("act", it, mb, dev)
+            if n_mb + 1 < len(mbs):
+                log.prefetch("act", it, mbs[n_mb + 1], dev)
         if first:
             x = synth_inputs(seed, it, mb, rows, dim, device=dev)
         else:
