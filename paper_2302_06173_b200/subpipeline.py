@@ -60,6 +60,8 @@ class SubPipeline:
     def __init__(self, stages: Sequence[Stage], m: int, rows: int, dim: int, group=None):
         from .recovery import _PEER_MAPS, _export
         self.stages = list(stages)
+        if not self.stages:
+            raise RwError(18, "InvalidConfig: every sub-pipeline worker needs at least one stage (p >= d)")
         self.m, self.rows, self.dim, self.group = m, rows, dim, group
         self.d, self.w = dist.get_world_size(group), dist.get_rank(group)
         self.dev = self.stages[0].device
