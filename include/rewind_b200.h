@@ -317,6 +317,15 @@ int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* act
  * CTA behind a collective kernel.  Process-wide. */
 int rw_replay_set_sm_reserve(int32_t n);
 
+/* Replay GEMM engine (process-wide; -1 keeps the default / environment):
+ *   epilogue: 1 = output tiles staged in shared memory and written by TMA
+ *             tensor stores (default), 0 = per-thread register stores;
+ *   pair:     1 = CTA-pair kernel (tcgen05 cta_group::2, M = 256),
+ *             0 = single-CTA kernel (default).
+ * Every combination gives the same bits (same MMA order, same epilogue
+ * arithmetic); the knob exists for A/B measurements and tests. */
+int rw_replay_set_gemm_engine(int32_t epilogue, int32_t pair);
+
 /* mse_loss (model.cpp:174-188): grad = 2/(n*micro_batches) * (pred - target)
  * (bf16 out); *loss (device double, may be NULL) = mean squared error.
  * scratch: 256 doubles. */

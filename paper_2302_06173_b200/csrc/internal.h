@@ -136,6 +136,7 @@ int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, co
 int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
                        int accumulate, void* stream);
 int replay_set_sm_reserve(int n);
+int replay_set_gemm_engine(int epilogue, int pair);
 // first-layer dgrad of stage k fused with stage k-1's dz: bf16(dX) * (1 - y^2)
 int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
                           const void* y_prev_stage, void* dz_prev_stage, void* stream);

@@ -113,6 +113,7 @@ int rw_mse_grad(const void* pred, const float* target, uint64_t n, uint64_t micr
 }
 
 int rw_replay_set_sm_reserve(int32_t n) { return rwb::replay_set_sm_reserve(n); }
+int rw_replay_set_gemm_engine(int32_t epilogue, int32_t pair) { return rwb::replay_set_gemm_engine(epilogue, pair); }
 
 int rw_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream) {
   rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(in));

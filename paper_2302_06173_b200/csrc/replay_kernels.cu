@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 #include "umma_gemm_host.h"
@@ -22,6 +23,7 @@ namespace {
 
 using bf16 = __nv_bfloat16;
 constexpr int kBN = 256;
+constexpr int kPairDefault = 0;
 
 __global__ void dtanh_first_kernel(const bf16* __restrict__ g, const bf16* __restrict__ y,
                                    bf16* __restrict__ dz, uint64_t n) {
@@ -115,6 +117,31 @@ static int gemm_cap() {
   return sms - g_sm_reserve > 1 ? sms - g_sm_reserve : 1;
 }
 
+// GEMM engine: the single-CTA kernel (cta_group::1, M128) or the CTA-pair
+// kernel (cta_group::2, M256: each SM stages half of the B tile, so L2->SM
+// traffic per FLOP drops by a third).  RW_GEMM_PAIR=0/1 overrides the default.
+static int g_pair_override = -1;
+static bool use_pair() {
+  if (g_pair_override >= 0) return g_pair_override != 0;
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RW_GEMM_PAIR");
+    v = (e && *e) ? (std::atoi(e) != 0) : kPairDefault;
+  }
+  return v != 0;
+}
+int replay_set_gemm_engine(int epilogue, int pair) {
+  gemm::tma_epi_override() = epilogue < 0 ? -1 : (epilogue != 0);
+  g_pair_override = pair < 0 ? -1 : (pair != 0);
+  return 0;
+}
+template <int AM, int BMJ, int EPI>
+static int gemm_run(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
+                    const gemm::EpiArgs& ep, cudaStream_t st) {
+  if (use_pair()) return gemm::launch2<kBN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, st, gemm_cap());
+  return gemm::launch<kBN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, st, gemm_cap());
+}
+
 int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, const void* w, const float* b,
                          void* y, void* stream) {
   gemm::EpiArgs ep{};
@@ -122,8 +149,8 @@ int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, c
   ep.ldo = out;
   ep.bias = b;
   // Y[R,out] = X[R,in] . W[in,out]: A = X (K-major), B = W viewed [out,in] (MN-major)
-  return gemm::launch<kBN, gemm::K_MAJOR, gemm::MN_MAJOR, gemm::EPI_BIAS_TANH_BF16>(
-      x, in, w, out, int(rows), int(out), int(in), ep, static_cast<cudaStream_t>(stream), gemm_cap());
+  return gemm_run<gemm::K_MAJOR, gemm::MN_MAJOR, gemm::EPI_BIAS_TANH_BF16>(
+      x, in, w, out, int(rows), int(out), int(in), ep, static_cast<cudaStream_t>(stream));
 }
 
 int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
@@ -136,10 +163,10 @@ int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, co
   auto st = static_cast<cudaStream_t>(stream);
   // dX[R,in] = dZ[R,out] . W[in,out]^T: A = dZ (K-major), B = W as [in,out] (K-major)
   if (y_prev)
-    return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_DTANH_BF16>(dz, out, w, out, int(rows),
-                                                                                 int(in), int(out), ep, st, gemm_cap());
-  return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BF16>(dz, out, w, out, int(rows), int(in),
-                                                                         int(out), ep, st, gemm_cap());
+    return gemm_run<gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_DTANH_BF16>(dz, out, w, out, int(rows),
+                                                                                 int(in), int(out), ep, st);
+  return gemm_run<gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BF16>(dz, out, w, out, int(rows), int(in),
+                                                                         int(out), ep, st);
 }
 
 int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
@@ -149,8 +176,8 @@ int replay_dgrad_boundary(const void* dz, int64_t rows, int64_t in, int64_t out,
   ep.ldo = in;
   ep.y = static_cast<const bf16*>(y_prev_stage);
   ep.ldy = in;
-  return gemm::launch<kBN, gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BOUNDARY_DTANH_BF16>(
-      dz, out, w, out, int(rows), int(in), int(out), ep, static_cast<cudaStream_t>(stream), gemm_cap());
+  return gemm_run<gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BOUNDARY_DTANH_BF16>(
+      dz, out, w, out, int(rows), int(in), int(out), ep, static_cast<cudaStream_t>(stream));
 }
 
 int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
@@ -161,10 +188,10 @@ int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, 
   auto st = static_cast<cudaStream_t>(stream);
   // dW[in,out] = X[R,in]^T . dZ[R,out]: A(m=in,k=r) = X[r,m] (MN-major), B(n=out,k=r) = dZ[r,n] (MN-major)
   if (accumulate)
-    return gemm::launch<kBN, gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32_ACC>(x, in, dz, out, int(in), int(out),
-                                                                                int(rows), ep, st, gemm_cap());
-  return gemm::launch<kBN, gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32>(x, in, dz, out, int(in), int(out),
-                                                                          int(rows), ep, st, gemm_cap());
+    return gemm_run<gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32_ACC>(x, in, dz, out, int(in), int(out),
+                                                                                int(rows), ep, st);
+  return gemm_run<gemm::MN_MAJOR, gemm::MN_MAJOR, gemm::EPI_F32>(x, in, dz, out, int(in), int(out),
+                                                                          int(rows), ep, st);
 }
 
 int replay_dtanh_first(const void* g, const void* y, void* dz, uint64_t n, void* stream) {

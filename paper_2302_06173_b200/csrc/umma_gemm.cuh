@@ -50,7 +50,11 @@ struct EpiArgs {
   const float* bias;     // [N] (EPI_BIAS_TANH_BF16)
   const __nv_bfloat16* y;  // [M, N] row-major, ld ldy (EPI_DTANH_BF16)
   int64_t ldy;
+  int tma_epi;           // set by the launcher: output (and y / old output) tiles move by TMA
 };
+__host__ __device__ constexpr bool epi_f32(int epi) { return epi == EPI_F32 || epi == EPI_F32_ACC; }
+// epilogues that read an [M, N] tile besides the accumulator (y, or the old output)
+__host__ __device__ constexpr bool epi_input(int epi) { return uses_y(epi) || epi == EPI_F32_ACC; }
 
 // ---------------------------------------------------------------- PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -95,6 +99,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+// smem -> global tensor store (bulk group), and the group waits
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy smem writes -> visible to the async proxy (TMA store source)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -251,6 +272,9 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
 #pragma unroll
         for (int j = 0; j < 32; ++j) w[j] = v[j];
       }
+#ifdef RWB_PROBE_NOSTORE
+      if (w[0] != 12345.f) return;  // probe only: compute everything, store (almost) nothing
+#endif
       if (col0 + 32 <= N) {
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
@@ -299,6 +323,130 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, int n0, i
   }
 }
 
+// ---------------------------------------------------------------- TMA epilogue
+// Each epilogue warp owns 32 accumulator rows and two 32-row x 128-byte
+// staging boxes in shared memory (128-byte swizzle: the 16-byte piece p of
+// row r sits at piece p ^ (r % 8), so a warp's row-per-lane accesses are
+// bank-conflict free).  A box holds 64 bf16 or 32 fp32 output columns; it
+// leaves by one TMA tensor store (full 128-byte lines, clipped at the matrix
+// edge), while the other box is being filled.  Epilogues with an input tile
+// (y of the dtanh epilogues, the old output of the fp32 accumulate) TMA-load
+// it into the box one box ahead and compute in place.
+constexpr uint32_t kEpiBoxBytes = 32 * 128;
+constexpr uint32_t kEpiSmem = 4 * 2 * kEpiBoxBytes;  // 4 warps x double buffer
+
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t piece) {
+  return row * 128u + ((piece ^ (row & 7u)) << 4);
+}
+__device__ __forceinline__ void epi_load_box(const CUtensorMap* mi, uint8_t* buf, uint64_t* bar, int c0, int r0) {
+  mbar_expect_tx(bar, kEpiBoxBytes);
+  tma_load_2d(buf, mi, bar, c0, r0);
+}
+
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0, int N, const EpiArgs& ep,
+                                                  const CUtensorMap* mo, const CUtensorMap* mi, uint8_t* ebuf,
+                                                  uint64_t* ebar, uint32_t& seq) {
+  constexpr int COLS = epi_f32(EPI) ? 32 : 64;
+  constexpr int NB = BN / COLS;
+  const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll 1
+  for (int i = 0; i < NB; ++i, ++seq) {
+    const uint32_t b = seq & 1u;
+    uint8_t* buf = ebuf + b * kEpiBoxBytes;
+    const int c0 = n0 + i * COLS;
+    if constexpr (epi_input(EPI)) {
+      if (i + 1 < NB && lane == 0) {  // next box's input, into the other buffer once its store has read it
+        bulk_wait_read<0>();
+        epi_load_box(mi, ebuf + (b ^ 1u) * kEpiBoxBytes, &ebar[b ^ 1u], c0 + COLS, r0);
+      }
+      mbar_wait(&ebar[b], (seq >> 1) & 1u);
+    } else {
+      if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read it
+      __syncwarp();
+    }
+#pragma unroll
+    for (int h = 0; h < COLS / 32; ++h) {
+      float v[32];
+      tmem_ld_32cols(tbase + uint32_t(i * COLS + h * 32), v);
+      if constexpr (epi_f32(EPI)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4* p = reinterpret_cast<float4*>(buf + swz(lane, q));
+          float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if constexpr (EPI == EPI_F32_ACC) {
+            const float4 o = *p;
+            w.x = __fadd_rn(o.x, w.x);
+            w.y = __fadd_rn(o.y, w.y);
+            w.z = __fadd_rn(o.z, w.z);
+            w.w = __fadd_rn(o.w, w.w);
+          }
+          *p = w;
+        }
+      } else {
+        const int col = c0 + h * 32;
+        float w[32];
+        if constexpr (EPI == EPI_BIAS_TANH_BF16) {
+          float bv[32];
+          if (col + 32 <= N) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(ep.bias + col + j));
+              bv[j] = b4.x;
+              bv[j + 1] = b4.y;
+              bv[j + 2] = b4.z;
+              bv[j + 3] = b4.w;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) bv[j] = (col + j < N) ? __ldg(ep.bias + col + j) : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j) w[j] = tanhf(__fadd_rn(v[j], bv[j]));
+        } else if constexpr (uses_y(EPI)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 u = *reinterpret_cast<const uint4*>(buf + swz(lane, h * 4 + q));
+            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 y2 = __bfloat1622float2(p2[e]);
+              const int j = q * 8 + 2 * e;
+              const float g0 = EPI == EPI_BOUNDARY_DTANH_BF16 ? __bfloat162float(__float2bfloat16_rn(v[j])) : v[j];
+              const float g1 =
+                  EPI == EPI_BOUNDARY_DTANH_BF16 ? __bfloat162float(__float2bfloat16_rn(v[j + 1])) : v[j + 1];
+              w[j] = __fmul_rn(g0, __fsub_rn(1.f, __fmul_rn(y2.x, y2.x)));
+              w[j + 1] = __fmul_rn(g1, __fsub_rn(1.f, __fmul_rn(y2.y, y2.y)));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) w[j] = v[j];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk;
+          __nv_bfloat162 h0 = __floats2bfloat162_rn(w[8 * q], w[8 * q + 1]);
+          __nv_bfloat162 h1 = __floats2bfloat162_rn(w[8 * q + 2], w[8 * q + 3]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(w[8 * q + 4], w[8 * q + 5]);
+          __nv_bfloat162 h3 = __floats2bfloat162_rn(w[8 * q + 6], w[8 * q + 7]);
+          pk.x = *reinterpret_cast<uint32_t*>(&h0);
+          pk.y = *reinterpret_cast<uint32_t*>(&h1);
+          pk.z = *reinterpret_cast<uint32_t*>(&h2);
+          pk.w = *reinterpret_cast<uint32_t*>(&h3);
+          *reinterpret_cast<uint4*>(buf + swz(lane, h * 4 + q)) = pk;
+        }
+      }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(mo, buf, c0, r0);
+      bulk_commit();
+    }
+  }
+}
+
 // Grouped tile rasterization: consecutive tile ids walk GM M-tiles down one
 // N column before moving right, so the ~148 concurrently active tiles cover a
 // compact GM x (148/GM) block whose A and B panels stay resident in the
@@ -316,28 +464,40 @@ constexpr int kGroupM = 16;
 
 template <int BN>
 struct Cfg {
+#ifdef RWB_GEMM_STAGES
+  static constexpr int kStages = RWB_GEMM_STAGES;
+#else
   static constexpr int kStages = BN == 256 ? 4 : 6;
+#endif
   static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB
   static constexpr uint32_t kBBytes = BN * BK * 2;   // 32 KB (BN=256)
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = 2 * BN;      // two accumulator stages
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024;  // + alignment slack
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmem + 1024;  // + alignment slack
 };
 
 // smem layout inside one operand buffer for MN-major tiles: TMA boxes of
 // {64 (MN), 64 (K)} stacked along MN every 64*128 B = 8 KB  => LBO = 8192.
 constexpr uint32_t kMnChunkBytes = 64 * 128;
 
+#ifdef RWB_PAIR_EXPERIMENT
+// tools/pair_probe.cu / tools/gemm_probe.cu instrumentation (per CTA):
+// [0] MMA-warp cycles waiting on full_bar, [1] on tempty_bar, [2] total MMA
+// loop cycles, [3] producer cycles waiting on empty_bar
+__device__ long long g_pair_dbg[148][4];
+#endif
+
 template <int BN, int AMAJ, int BMAJ, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     umma_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                     const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ CUtensorMap tma_i,
                      int M, int N, int K, EpiArgs ep) {
   using C = Cfg<BN>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base for the swizzled tiles
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2], epi_bar[8];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -355,6 +515,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 4);  // one arrive per epilogue warp
+    }
+    for (int i = 0; i < 8; ++i) mbar_init(&epi_bar[i], 1);
+    if (ep.tma_epi) {
+      prefetch_tmap(&tma_o);
+      if (epi_input(EPI)) prefetch_tmap(&tma_i);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -379,9 +544,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tile_coords(tile, tiles_m, tiles_n, kGroupM, tm, tn);
         const int m0 = tm * BM, n0 = tn * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef RWB_PAIR_EXPERIMENT
+          const long long w0 = clock64();
+#endif
           mbar_wait(&empty_bar[stage], phase ^ 1);
+#ifdef RWB_PAIR_EXPERIMENT
+          g_pair_dbg[blockIdx.x][3] += clock64() - w0;
+#endif
           uint8_t* sa = smem + stage * C::kStageBytes;
           uint8_t* sb = sa + C::kABytes;
+#ifdef RWB_PROBE_NOTMA
+          if (tile != int(blockIdx.x) || kb >= S) {  // probe only: no data movement after the first fill
+            mbar_arrive(&full_bar[stage]);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+#endif
           mbar_expect_tx(&full_bar[stage], C::kStageBytes);
           const int k0 = kb * BK;
           if constexpr (AMAJ == K_MAJOR) {
@@ -412,12 +593,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+#ifdef RWB_PAIR_EXPERIMENT
+    const long long l0 = clock64();
+#endif
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+#ifdef RWB_PAIR_EXPERIMENT
+      const long long a0 = clock64();
+#endif
       mbar_wait(&tempty_bar[acc], acc_phase ^ 1);  // epilogue drained this accumulator
+#ifdef RWB_PAIR_EXPERIMENT
+      if (lane == 0) g_pair_dbg[blockIdx.x][1] += clock64() - a0;
+#endif
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
       for (int kb = 0; kb < num_kb; ++kb) {
+#ifdef RWB_PAIR_EXPERIMENT
+        const long long f0 = clock64();
+#endif
         mbar_wait(&full_bar[stage], phase);
+#ifdef RWB_PAIR_EXPERIMENT
+        if (lane == 0) g_pair_dbg[blockIdx.x][0] += clock64() - f0;
+#endif
         tc_fence_after();
         if (lane == 0) {
           const uint32_t sa = smem_u32(smem + stage * C::kStageBytes);
@@ -447,9 +643,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+#ifdef RWB_PAIR_EXPERIMENT
+    if (lane == 0) g_pair_dbg[blockIdx.x][2] += clock64() - l0;
+#endif
   } else if (warp >= kEpiWarp0) {
     // ===================== epilogue (warps 4..7 -> TMEM lanes 0..127) =====================
     const int ew = warp - kEpiWarp0;  // == warp % 4: TMEM lane quarter this warp may access
+    uint8_t* ebuf = smem + S * C::kStageBytes + ew * 2 * kEpiBoxBytes;
+    uint64_t* ebar = &epi_bar[ew * 2];
+    uint32_t seq = 0;  // boxes this warp has staged so far (buffer = seq % 2)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -457,12 +659,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_coords(tile, tiles_m, tiles_n, kGroupM, tm, tn);
       const int m0 = tm * BM, n0 = tn * BN;
       const int row = m0 + ew * 32 + lane;
-      YChunk y0;
-      if constexpr (uses_y(EPI)) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
-      epilogue_tile<BN, EPI>(tbase, row, n0, M, N, ep, &y0);
+#ifdef RWB_PROBE_EPI_SKIP
+      if (true) {  // probe only: release the accumulator without reading it
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+      } else
+#endif
+      if (ep.tma_epi) {
+        if constexpr (epi_input(EPI)) {  // the tile's first input box overlaps the wait
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], n0, m0 + ew * 32);
+          }
+        }
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        epilogue_tile_tma<BN, EPI>(tbase, m0 + ew * 32, n0, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+      } else {
+        YChunk y0;
+        if constexpr (uses_y(EPI)) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        epilogue_tile<BN, EPI>(tbase, row, n0, M, N, ep, &y0);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty_bar[acc]);
@@ -471,6 +691,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (ep.tma_epi && lane == 0) bulk_wait_all();  // the last stores have landed
   }
   __syncthreads();
   if (warp == 2) {
@@ -534,27 +755,26 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
       : "memory");
 }
 
-#ifdef RWB_PAIR_EXPERIMENT
-// tools/gemm_test.cu instrumentation of the parked pair kernel (per CTA):
-// [0] MMA-warp cycles waiting on full_bar, [1] on tempty_bar, [2] total MMA
-// loop cycles, [3] producer cycles waiting on empty_bar
-__device__ long long g_pair_dbg[148][4];
-#endif
 
 template <int BN>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;
+#ifdef RWB_GEMM2_STAGES
+  static constexpr int kStages = RWB_GEMM2_STAGES;
+#else
   static constexpr int kStages = 6;
+#endif
   static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB: this CTA's 128 rows
   static constexpr uint32_t kBBytes = BNH * BK * 2;  // 16 KB: half of the B tile
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = 2 * BN;
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + 1024;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmem + 1024;
 };
 
 template <int BN, int AMAJ, int BMAJ, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     umma_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                      const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ CUtensorMap tma_i,
                       int M, int N, int K, EpiArgs ep) {
   using C = Cfg2<BN>;
   constexpr int S = C::kStages;
@@ -562,7 +782,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr int PM = 2 * BM;  // rows per CTA pair
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2];
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2], epi_bar[8];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -583,6 +803,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    for (int i = 0; i < 8; ++i) mbar_init(&epi_bar[i], 1);
+    if (ep.tma_epi) {
+      prefetch_tmap(&tma_o);
+      if (epi_input(EPI)) prefetch_tmap(&tma_i);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -717,18 +942,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================== epilogue (both CTAs, own 128 rows) =====================
     const int ew = warp - kEpiWarp0;
     const uint32_t tempty_leader = mapa_rank0(smem_u32(&tempty_bar[0]));
+    uint8_t* ebuf = smem + S * C::kStageBytes + ew * 2 * kEpiBoxBytes;
+    uint64_t* ebar = &epi_bar[ew * 2];
+    uint32_t seq = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl) {
       int tm, tn;
       tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
-      const int row = tm * PM + int(rank) * BM + ew * 32 + lane;
-      YChunk y0;
-      if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
+      const int r0 = tm * PM + int(rank) * BM + ew * 32;
+      const int row = r0 + lane;
       const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
-      epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
+      if (ep.tma_epi) {
+        if constexpr (epi_input(EPI)) {
+          if (lane == 0) {
+            bulk_wait_read<0>();
+            epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], tn * BN, r0);
+          }
+        }
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        epilogue_tile_tma<BN, EPI>(tbase, r0, tn * BN, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+      } else {
+        YChunk y0;
+        if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
@@ -737,6 +978,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (ep.tma_epi && lane == 0) bulk_wait_all();
   }
   __syncthreads();
   cluster_sync();

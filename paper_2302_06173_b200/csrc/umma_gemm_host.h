@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "umma_gemm.cuh"
 
@@ -44,6 +45,38 @@ inline int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
 }
 
+// Epilogue staging box map: [rows, cols] row-major, element size esize, box
+// {128 bytes of columns, 32 rows}, 128-byte swizzle.  Fails (non-zero) when
+// the matrix cannot be a TMA operand (base not 16-byte aligned, pitch not a
+// multiple of 16 bytes); the launcher then keeps the register epilogue.
+inline int make_epi_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld, int esize) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15u) || ((ld * esize) & 15u)) return 1;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * esize};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / esize), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, esize == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : 1;
+}
+
+// RW_GEMM_TMA_EPI=0 keeps the register epilogue (A/B measurements)
+inline int& tma_epi_override() {  // -1: environment / default; 0 / 1 forced (tests)
+  static int v = -1;
+  return v;
+}
+inline bool tma_epi_enabled() {
+  if (tma_epi_override() >= 0) return tma_epi_override() != 0;
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("RW_GEMM_TMA_EPI");
+    v = (e && *e) ? (std::atoi(e) != 0) : 1;
+  }
+  return v != 0;
+}
+
 // C[M,N] (+)= A . B^T with A given as [M,K] (K_MAJOR) or [K,M] (MN_MAJOR) and
 // B as [N,K] (K_MAJOR) or [K,N] (MN_MAJOR); lda/ldb = row pitch in elements.
 template <int BN, int AMAJ, int BMAJ, int EPI>
@@ -54,6 +87,15 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
   if (e) return e;
   e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN) : make_map(&mb, B, K, N, ldb, 64);
   if (e) return e;
+  EpiArgs epx = ep;
+  CUtensorMap mo{}, mi{};
+  {
+    constexpr int es = epi_f32(EPI) ? 4 : 2;
+    bool ok = tma_epi_enabled() && make_epi_map(&mo, ep.out, M, N, ep.ldo, es) == 0;
+    if (ok && uses_y(EPI)) ok = make_epi_map(&mi, ep.y, M, N, ep.ldy, 2) == 0;
+    if (ok && EPI == EPI_F32_ACC) mi = mo;
+    epx.tma_epi = ok ? 1 : 0;
+  }
   auto kern = umma_gemm_kernel<BN, AMAJ, BMAJ, EPI>;
   static unsigned long long dev_mask = 0;  // the attribute is per device
   int cur_dev = 0;
@@ -70,7 +112,7 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   int grid = tiles < sms ? tiles : sms;
   if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-  kern<<<grid, kThreads, Cfg<BN>::kSmem, stream>>>(ma, mb, M, N, K, ep);
+  kern<<<grid, kThreads, Cfg<BN>::kSmem, stream>>>(ma, mb, mo, mi, M, N, K, epx);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -83,6 +125,15 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
   if (e) return e;
   e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN / 2) : make_map(&mb, B, K, N, ldb, 64);
   if (e) return e;
+  EpiArgs epx = ep;
+  CUtensorMap mo{}, mi{};
+  {
+    constexpr int es = epi_f32(EPI) ? 4 : 2;
+    bool ok = tma_epi_enabled() && make_epi_map(&mo, ep.out, M, N, ep.ldo, es) == 0;
+    if (ok && uses_y(EPI)) ok = make_epi_map(&mi, ep.y, M, N, ep.ldy, 2) == 0;
+    if (ok && EPI == EPI_F32_ACC) mi = mo;
+    epx.tma_epi = ok ? 1 : 0;
+  }
   auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI>;
   static unsigned long long dev_mask = 0;  // the attribute is per device
   int cur_dev = 0;
@@ -100,7 +151,7 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
   int pairs = sms / 2;
   if (tiles < pairs) pairs = tiles;
   if (max_ctas > 0 && pairs * 2 > max_ctas) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
-  kern<<<pairs * 2, kThreads, Cfg2<BN>::kSmem, stream>>>(ma, mb, M, N, K, ep);
+  kern<<<pairs * 2, kThreads, Cfg2<BN>::kSmem, stream>>>(ma, mb, mo, mi, M, N, K, epx);
   return static_cast<int>(cudaGetLastError());
 }
 

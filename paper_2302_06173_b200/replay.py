@@ -51,6 +51,7 @@ _sig = {
                               C.c_void_p, C.c_void_p]),
     "rw_cast_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "rw_replay_set_sm_reserve": (C.c_int, [C.c_int32]),
+    "rw_replay_set_gemm_engine": (C.c_int, [C.c_int32, C.c_int32]),
 }
 for _n, (_r, _a) in _sig.items():
     _f = getattr(LIB, _n)

@@ -41,12 +41,34 @@ def _free_port():
     return p
 
 
+def _to_wire(obj):
+    """Tensors leave a worker as numpy arrays: a torch queue shares tensors by
+    file descriptor, and the worker may exit before the parent receives."""
+    if isinstance(obj, torch.Tensor):
+        return ("__tensor__", obj.detach().cpu().numpy().copy())
+    if isinstance(obj, dict):
+        return {k: _to_wire(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return type(obj)(_to_wire(v) for v in obj)
+    return obj
+
+
+def _from_wire(obj):
+    if isinstance(obj, tuple) and len(obj) == 2 and obj[0] == "__tensor__":
+        return torch.from_numpy(obj[1])
+    if isinstance(obj, dict):
+        return {k: _from_wire(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return type(obj)(_from_wire(v) for v in obj)
+    return obj
+
+
 def _worker(rank, world, port, scenario, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         out = scenario(rank)
-        q.put((rank, out))
+        q.put((rank, _to_wire(out)))
     finally:
         dist.destroy_process_group()
 
@@ -58,7 +80,7 @@ def _run(scenario, world=2):
     ps = [ctx.Process(target=_worker, args=(r, world, port, scenario, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = dict(q.get(timeout=120) for _ in ps)
+    res = {r: _from_wire(o) for r, o in (q.get(timeout=120) for _ in ps)}
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0

@@ -99,6 +99,37 @@ def test_backward_is_deterministic():
         assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
 
 
+@pytest.mark.parametrize("rows,din,dh,dout", [(512, 256, 512, 256), (200, 96, 264, 56)])
+def test_gemm_engines_agree_bitwise(rows, din, dh, dout):
+    """The four GEMM engines (TMA-staged or register epilogue x single-CTA or
+    CTA-pair kernel) give the same bits for forward, backward with a fused
+    stage boundary, and the accumulated fp32 weight gradients (second
+    micro-batch: EPI_F32_ACC); the ragged shape exercises clipped TMA boxes."""
+    from paper_2302_06173_b200.replay import LIB
+    from paper_2302_06173_b200._lib import check
+    results = []
+    try:
+        for epi, pair in ((1, 0), (0, 0), (1, 1), (0, 1)):
+            check(LIB.rw_replay_set_gemm_engine(epi, pair))
+            st = Stage(3, din, dh, dout, 2, 5, ADAM)
+            prev = synth_inputs(5, 0, 9, rows, din)  # stands for the previous stage's output
+            outs = []
+            for mb in range(2):
+                acts = st.new_acts(rows, synth_inputs(5, 0, mb, rows, din))
+                st.forward(acts)
+                g = synth_inputs(5, 1, mb, rows, dout)
+                gout = torch.empty(rows, din, dtype=torch.bfloat16, device="cuda")
+                st.backward(acts, g, gout, accumulate=mb > 0, prev_y=prev)
+                outs += [acts[1].clone(), acts[2].clone(), gout]
+            torch.cuda.synchronize()
+            results.append(outs + [st.grad.clone()])
+    finally:
+        check(LIB.rw_replay_set_gemm_engine(-1, -1))
+    for other in results[1:]:
+        for a, b in zip(results[0], other):
+            assert torch.equal(a, b)
+
+
 def _pipeline(kind=ADAM):
     h = OptimizerHyper(kind=kind, lr=1e-3 if kind == ADAM else 0.05, weight_decay=0.01)
     return Pipeline(p=3, dim=64, hidden=128, layers=2, rows=128, micro_batches=4, seed=11, kind=kind,

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "umma_gemm_host.h"
@@ -107,12 +108,31 @@ bool check(const char* name, int M, int N, int K) {
     CK(cudaMemcpy(ho.data(), O, ho.size() * 2, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < ho.size(); ++i) hc[i] = __bfloat162float(ho[i]);
   }
+  // the TMA-staged epilogue must equal the register epilogue bit for bit
+  bool same = true;
+  {
+    tma_epi_override() = 0;
+    if (EPI == EPI_F32 || EPI == EPI_F32_ACC) CK(cudaMemset(C, 0, size_t(M) * N * 4));
+    run_gemm<BN, AM, BMJ, EPI, PAIR>(A, lda, B, ldb, M, N, K, ep, 0);
+    if (EPI == EPI_F32_ACC) run_gemm<BN, AM, BMJ, EPI, PAIR>(A, lda, B, ldb, M, N, K, ep, 0);
+    CK(cudaDeviceSynchronize());
+    tma_epi_override() = -1;
+    if (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
+      std::vector<float> h2(size_t(M) * N);
+      CK(cudaMemcpy(h2.data(), C, h2.size() * 4, cudaMemcpyDeviceToHost));
+      same = std::memcmp(h2.data(), hc.data(), h2.size() * 4) == 0;
+    } else {
+      std::vector<__nv_bfloat16> h2(size_t(M) * N);
+      CK(cudaMemcpy(h2.data(), O, h2.size() * 2, cudaMemcpyDeviceToHost));
+      same = std::memcmp(h2.data(), ho.data(), h2.size() * 2) == 0;
+    }
+  }
   double max_err = 0, max_ref = 0;
   for (size_t i = 0; i < hr.size(); ++i) {
     double ref = hr[i];
     const int n = int(i % N);
     if (EPI == EPI_BIAS_TANH_BF16) ref = std::tanh(ref + hb[n]);
-    if (EPI == EPI_DTANH_BF16) {
+    if (EPI == EPI_DTANH_BF16 || EPI == EPI_BOUNDARY_DTANH_BF16) {
       double y = __bfloat162float(hyb[i]);
       ref = ref * (1.0 - y * y);
     }
@@ -122,9 +142,9 @@ bool check(const char* name, int M, int N, int K) {
   }
   // bf16 output: ~2^-8 relative; fp32 accumulation-order differences ~1e-6
   const double tol = (EPI == EPI_F32 || EPI == EPI_F32_ACC) ? 1e-4 * max_ref + 1e-3 : 1e-2 * max_ref + 1e-2;
-  bool ok = max_err <= tol && std::isfinite(max_err);
-  printf("%-34s M=%5d N=%5d K=%5d  max|err|=%.3e  max|ref|=%.3e  %s\n", name, M, N, K, max_err, max_ref,
-         ok ? "OK" : "FAIL");
+  bool ok = max_err <= tol && std::isfinite(max_err) && same;
+  printf("%-34s M=%5d N=%5d K=%5d  max|err|=%.3e  max|ref|=%.3e  %s%s\n", name, M, N, K, max_err, max_ref,
+         ok ? "OK" : "FAIL", same ? "  (tma == register epilogue)" : "  (tma != register epilogue)");
   cudaFree(A);
   cudaFree(B);
   cudaFree(C);
@@ -188,6 +208,11 @@ int main(int argc, char** argv) {
   all &= check<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16>("dgrad *(1-y^2) bf16", 384, 512, 768);
   all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32_ACC>("wgrad f32 accumulate", 512, 256, 1024);
   all &= check<256, K_MAJOR, K_MAJOR, EPI_BF16>("KK bf16 big", 2048, 2048, 2048);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_BOUNDARY_DTANH_BF16>("boundary bf16(acc)*(1-y^2)", 384, 512, 768);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16>("dgrad dtanh ragged (TMA edge)", 200, 264, 136);
+  all &= check<256, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward ragged (TMA edge)", 200, 264, 136);
+  // (MN-major operands need M, N multiples of 8: a TMA row pitch is a multiple of 16 bytes)
+  all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32_ACC>("wgrad acc ragged (TMA edge)", 208, 296, 136);
   // CTA-pair (cta_group::2) kernel
   all &= check<256, K_MAJOR, K_MAJOR, EPI_F32, true>("PAIR KK f32", 512, 512, 256);
   all &= check<256, K_MAJOR, MN_MAJOR, EPI_F32, true>("PAIR K/MN f32", 512, 512, 256);
@@ -197,6 +222,9 @@ int main(int argc, char** argv) {
   all &= check<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16, true>("PAIR dgrad dtanh", 512, 512, 768);
   all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32_ACC, true>("PAIR wgrad accumulate", 512, 256, 1024);
   all &= check<256, K_MAJOR, K_MAJOR, EPI_BF16, true>("PAIR KK bf16 big", 2048, 2048, 2048);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_BOUNDARY_DTANH_BF16, true>("PAIR boundary", 512, 512, 768);
+  all &= check<256, K_MAJOR, K_MAJOR, EPI_DTANH_BF16, true>("PAIR dgrad dtanh ragged", 200, 264, 136);
+  all &= check<256, MN_MAJOR, MN_MAJOR, EPI_F32_ACC, true>("PAIR wgrad acc ragged", 208, 296, 136);
   printf("correctness: %s\n", all ? "ALL OK" : "FAILURES");
   if (argc > 1) {
     perf<256, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward 16384x16384x4096", 16384, 16384, 4096);

@@ -3,6 +3,8 @@
 // operands SS from zeroed smem, whole GPU loaded (74 clusters of 2).
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2302_06173_b200/csrc \
 //        tools/mma_rate.cu -o tools/mma_rate -lcuda
+#include <cuda_bf16.h>
+
 #include <cstdio>
 
 #include "umma_gemm.cuh"
@@ -19,13 +21,25 @@ __device__ __forceinline__ void csync() {
 }
 
 template <int CG, int N>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma_rate(int iters, long long* out) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma_rate(int iters, long long* out, int rnd) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(smem)[i] = 0;
+  for (int i = threadIdx.x; i < 65536 / 4; i += blockDim.x) {
+    uint32_t w = 0;
+    if (rnd) {  // two random bf16 in [-0.5, 0.5): real-data switching activity
+      uint32_t h = uint32_t(i + blockIdx.x * 65536) * 2654435761u;
+      h ^= h >> 15;
+      h *= 2246822519u;
+      h ^= h >> 13;
+      const __nv_bfloat16 a = __float2bfloat16(float(h & 0xffff) / 65536.f - 0.5f);
+      const __nv_bfloat16 b = __float2bfloat16(float(h >> 16) / 65536.f - 0.5f);
+      w = uint32_t(*reinterpret_cast<const uint16_t*>(&a)) | (uint32_t(*reinterpret_cast<const uint16_t*>(&b)) << 16);
+    }
+    reinterpret_cast<uint32_t*>(smem)[i] = w;
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -96,20 +110,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) mma_rate(int
 }
 
 template <int CG, int N>
-void run(const char* name) {
+void run(const char* name, int rnd) {
   const int iters = 20000, grid = 148;
   long long* d;
   cudaMalloc(&d, grid * sizeof(long long));
   cudaMemset(d, 0, grid * sizeof(long long));
   auto k = mma_rate<CG, N>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 66 * 1024);
-  k<<<grid, 128, 66 * 1024>>>(100, d);
+  k<<<grid, 128, 66 * 1024>>>(100, d, rnd);
   cudaDeviceSynchronize();
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  k<<<grid, 128, 66 * 1024>>>(iters, d);
+  k<<<grid, 128, 66 * 1024>>>(iters, d, rnd);
   cudaEventRecord(e1);
   cudaError_t err = cudaDeviceSynchronize();
   float ms = 0;
@@ -120,15 +134,17 @@ void run(const char* name) {
   for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
   const double n_instr = double(iters) * 4;
   const double flop = n_instr * 2.0 * (CG == 2 ? 256 : 128) * N * 16 * (CG == 2 ? grid / 2 : grid);
-  printf("%-28s err=%d  cycles/instr(issuer)=%.1f  %.3f ms  %.1f TFLOP/s\n", name, int(err), double(mx) / n_instr,
+  printf("%-28s %s err=%d  cycles/instr(issuer)=%.1f  %.3f ms  %.1f TFLOP/s\n", name, rnd ? "random" : "zeros ", int(err), double(mx) / n_instr,
          ms, flop / (ms * 1e-3) / 1e12);
   cudaFree(d);
 }
 
 int main() {
-  run<1, 256>("cta_group::1 M128 N256");
-  run<1, 128>("cta_group::1 M128 N128");
-  run<2, 256>("cta_group::2 M256 N256");
-  run<2, 128>("cta_group::2 M256 N128");
+  for (int rnd = 0; rnd < 2; ++rnd) {
+    run<1, 256>("cta_group::1 M128 N256", rnd);
+    run<1, 128>("cta_group::1 M128 N128", rnd);
+    run<2, 256>("cta_group::2 M256 N256", rnd);
+    run<2, 128>("cta_group::2 M256 N128", rnd);
+  }
   return 0;
 }
