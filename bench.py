@@ -957,6 +957,10 @@ def run_b200(args) -> None:
             r = cpu_reference_undo(seconds_target=1.0, steps=3, warmup=1)
             cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
             cpu["params_per_s"] = r["params_per_s"]
+            # the reference as it runs (one thread) beside the all-core number
+            r1 = cpu_reference_undo(seconds_target=0.5, threads=1, steps=1, warmup=0)
+            cpu["one_thread"] = dict(value=round(r1["value"], 3), params_per_s=round(r1["params_per_s"], 1),
+                                     own_bytes_gbs=round(r1["own_bytes_gbs"], 3), params=r1["params"])
             if not args.no_extras:  # the same reference, for the recovery and replay extras
                 if "recovery" in extras:
                     extras["recovery"]["cpu_reference"] = cpu_reference_recovery(r["params_per_s"])
