@@ -834,7 +834,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = tmem_base_sh;
 
   if (warp == 0) {
-    // ===================== TMA producer (both CTAs) =====================
+    // ===================== TMA producer =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
