@@ -311,6 +311,17 @@ int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* act
                          float* const* db, int32_t accumulate, void* scratch_dz0, void* scratch_dz1,
                          float* scratch_f32, void* stream);
 
+/* rw_stage_backward_ex with the fp32 scratch size stated (elements).  When it
+ * holds ceil(rows/32) * max(dims) floats, the column sums (db) of every dz that
+ * a dgrad GEMM produces are formed in that GEMM's epilogue (per 32-row block,
+ * from the bf16 values it stores) and only the ceil(rows/32) partial rows are
+ * summed afterwards (in row order), instead of re-reading dz; otherwise, and
+ * for the layer whose dz comes in, the separate column-sum pass runs. */
+int rw_stage_backward_ex2(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
+                          int32_t grad_in_is_dz, void* grad_out, const void* prev_y, float* const* dw,
+                          float* const* db, int32_t accumulate, void* scratch_dz0, void* scratch_dz1,
+                          float* scratch_f32, uint64_t scratch_f32_elems, void* stream);
+
 /* Keep n SMs free of the replay GEMM grids (0 = use every SM), so that
  * collectives issued concurrently (parallel-recovery merges) get SMs: the
  * persistent GEMM's static tile schedule would otherwise wait for its last

@@ -131,8 +131,15 @@ uint64_t crc32_scratch_words(uint64_t n);
 // replay_kernels.cu (all return cudaError_t as int)
 int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, const void* w, const float* b,
                          void* y, void* stream);
+// colsum (optional, y_prev != NULL): the epilogue also writes the per-32-row column
+// sums of dst, [ceil(rows/32), in] fp32 (fused db partials); *fused reports whether
+// it did (it cannot when the output is not a TMA operand or the engine is the
+// register epilogue), and then replay_colsum must run instead
 int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
-                       const void* y_prev, void* dst, void* stream);
+                       const void* y_prev, void* dst, void* stream, float* colsum = nullptr,
+                       int* fused = nullptr);
+// db (+)= the nsplit partial rows of part [nsplit, cols], summed in row order
+int replay_colsum_final(const float* part, int64_t nsplit, int64_t cols, float* db, int accumulate, void* stream);
 int replay_wgrad_layer(const void* x, const void* dz, int64_t rows, int64_t in, int64_t out, float* dw,
                        int accumulate, void* stream);
 int replay_set_sm_reserve(int n);

@@ -58,6 +58,18 @@ int rw_stage_backward(const rw_stage_desc* st, int64_t rows, void* const* acts, 
 int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
                          int32_t grad_in_is_dz, void* grad_out, const void* prev_y, float* const* dw,
                          float* const* db, int32_t accumulate, void* dz0, void* dz1, float* scratch, void* stream) {
+  int s = check_desc(st, rows);
+  if (s) return s;
+  int64_t mx = 0;
+  for (int l = 0; l <= st->num_layers; ++l) mx = st->dims[l] > mx ? st->dims[l] : mx;
+  return rw_stage_backward_ex2(st, rows, acts, grad_in, grad_in_is_dz, grad_out, prev_y, dw, db, accumulate, dz0,
+                               dz1, scratch, uint64_t(64) * uint64_t(mx), stream);
+}
+
+int rw_stage_backward_ex2(const rw_stage_desc* st, int64_t rows, void* const* acts, const void* grad_in,
+                          int32_t grad_in_is_dz, void* grad_out, const void* prev_y, float* const* dw,
+                          float* const* db, int32_t accumulate, void* dz0, void* dz1, float* scratch,
+                          uint64_t scratch_elems, void* stream) {
   rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(grad_in));
   int s = check_desc(st, rows);
   if (s) return s;
@@ -78,18 +90,27 @@ int rw_stage_backward_ex(const rw_stage_desc* st, int64_t rows, void* const* act
     e = rwb::replay_dtanh_first(grad_in, acts[L], cur, uint64_t(rows) * uint64_t(st->dims[L]), stream);
     if (e) return cfail(e, "dtanh");
   }
+  // db partials of the dz in `cur` already written by the GEMM that produced it
+  // (per 32-row block, into scratch) when the scratch holds ceil(rows/32) rows
+  const int64_t nsplit = (rows + 31) / 32;
+  bool cur_fused = false;
   for (int li = L - 1; li >= 0; --li) {  // reverse layer order (model.cpp:179)
     const int64_t in = st->dims[li], out = st->dims[li + 1];
     // dW = x^T dz (:193-203), accumulated over micro-batches in order
     e = rwb::replay_wgrad_layer(acts[li], cur, rows, in, out, dw[li], accumulate, stream);
     if (e) return cfail(e, "wgrad GEMM");
     // db = column sums of dz (:204-209)
-    e = rwb::replay_colsum(cur, rows, out, db[li], scratch, accumulate, stream);
+    e = cur_fused ? rwb::replay_colsum_final(scratch, nsplit, out, db[li], accumulate, stream)
+                  : rwb::replay_colsum(cur, rows, out, db[li], scratch, accumulate, stream);
     if (e) return cfail(e, "db colsum");
     // dx = dz W^T (:210-219); for li > 0 fuse the next layer's (1 - y^2)
+    // (and the column sums of the dz it produces)
     if (li > 0) {
-      e = rwb::replay_dgrad_layer(cur, rows, in, out, st->w[li], acts[li], nxt, stream);
+      int fused = 0;
+      float* part = uint64_t(nsplit) * uint64_t(in) <= scratch_elems ? scratch : nullptr;
+      e = rwb::replay_dgrad_layer(cur, rows, in, out, st->w[li], acts[li], nxt, stream, part, &fused);
       if (e) return cfail(e, "dgrad GEMM");
+      cur_fused = fused != 0;
       std::swap(cur, nxt);
     } else if (grad_out && prev_y) {  // dz of the previous stage (same GPU), bit-identical
       e = rwb::replay_dgrad_boundary(cur, rows, in, out, st->w[li], prev_y, grad_out, stream);

@@ -48,12 +48,12 @@ __global__ void colsum_partial_kernel(const bf16* __restrict__ dz, int64_t rows,
   for (int64_t r = r0; r < r1; ++r) acc = __fadd_rn(acc, __bfloat162float(dz[r * cols + c]));
   part[int64_t(s) * cols + c] = acc;
 }
-__global__ void colsum_final_kernel(const float* __restrict__ part, int64_t cols, float* __restrict__ db,
-                                    int accumulate) {
+__global__ void colsum_final_kernel(const float* __restrict__ part, int64_t nsplit, int64_t cols,
+                                    float* __restrict__ db, int accumulate) {
   const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (c >= cols) return;
   float acc = part[c];
-  for (int s = 1; s < kColSplit; ++s) acc = __fadd_rn(acc, part[int64_t(s) * cols + c]);
+  for (int64_t s = 1; s < nsplit; ++s) acc = __fadd_rn(acc, part[s * cols + c]);
   db[c] = accumulate ? __fadd_rn(db[c], acc) : acc;
 }
 
@@ -154,17 +154,30 @@ int replay_forward_layer(const void* x, int64_t rows, int64_t in, int64_t out, c
 }
 
 int replay_dgrad_layer(const void* dz, int64_t rows, int64_t in, int64_t out, const void* w,
-                       const void* y_prev, void* dst, void* stream) {
+                       const void* y_prev, void* dst, void* stream, float* colsum, int* fused) {
   gemm::EpiArgs ep{};
   ep.out = dst;
   ep.ldo = in;
   ep.y = static_cast<const bf16*>(y_prev);
   ep.ldy = in;
   auto st = static_cast<cudaStream_t>(stream);
+  if (fused) *fused = 0;
   // dX[R,in] = dZ[R,out] . W[in,out]^T: A = dZ (K-major), B = W as [in,out] (K-major)
-  if (y_prev)
+  if (y_prev) {
+    if (colsum && gemm::tma_epi_enabled()) {
+      ep.colsum = colsum;
+      ep.ldc = in;
+      const int e = gemm_run<gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_DTANH_BF16>(dz, out, w, out, int(rows),
+                                                                                 int(in), int(out), ep, st);
+      if (e != static_cast<int>(cudaErrorNotSupported)) {
+        if (fused && e == 0) *fused = 1;
+        return e;
+      }
+      ep.colsum = nullptr;  // not a TMA operand: plain epilogue, the caller sums the columns
+    }
     return gemm_run<gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_DTANH_BF16>(dz, out, w, out, int(rows),
                                                                                  int(in), int(out), ep, st);
+  }
   return gemm_run<gemm::K_MAJOR, gemm::K_MAJOR, gemm::EPI_BF16>(dz, out, w, out, int(rows), int(in),
                                                                          int(out), ep, st);
 }
@@ -205,7 +218,35 @@ int replay_colsum(const void* dz, int64_t rows, int64_t cols, float* db, float* 
   auto st = static_cast<cudaStream_t>(stream);
   dim3 g(unsigned((cols + 127) / 128), kColSplit);
   colsum_partial_kernel<<<g, 128, 0, st>>>(static_cast<const bf16*>(dz), rows, cols, scratch);
-  colsum_final_kernel<<<unsigned((cols + 127) / 128), 128, 0, st>>>(scratch, cols, db, accumulate);
+  colsum_final_kernel<<<unsigned((cols + 127) / 128), 128, 0, st>>>(scratch, kColSplit, cols, db, accumulate);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Many partial rows (the fused db partials, ceil(rows/32) of them): 8 row
+// lanes per column each sum a contiguous eighth in row order, then the eight
+// sums are added in lane order -- a fixed order, more loads in flight.
+__global__ void colsum_final8_kernel(const float* __restrict__ part, int64_t nsplit, int64_t cols,
+                                     float* __restrict__ db, int accumulate) {
+  __shared__ float sh[8][32];
+  const int64_t c = blockIdx.x * int64_t(32) + threadIdx.x;
+  const int j = threadIdx.y;
+  const int64_t s0 = nsplit * j / 8, s1 = nsplit * (j + 1) / 8;
+  float acc = 0.f;
+  if (c < cols)
+    for (int64_t s = s0; s < s1; ++s) acc = __fadd_rn(acc, part[s * cols + c]);
+  sh[j][threadIdx.x] = acc;
+  __syncthreads();
+  if (j == 0 && c < cols) {
+    float t = sh[0][threadIdx.x];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t = __fadd_rn(t, sh[q][threadIdx.x]);
+    db[c] = accumulate ? __fadd_rn(db[c], t) : t;
+  }
+}
+
+int replay_colsum_final(const float* part, int64_t nsplit, int64_t cols, float* db, int accumulate, void* stream) {
+  colsum_final8_kernel<<<unsigned((cols + 31) / 32), dim3(32, 8), 0, static_cast<cudaStream_t>(stream)>>>(
+      part, nsplit, cols, db, accumulate);
   return static_cast<int>(cudaGetLastError());
 }
 

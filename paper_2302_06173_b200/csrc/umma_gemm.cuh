@@ -51,6 +51,8 @@ struct EpiArgs {
   const __nv_bfloat16* y;  // [M, N] row-major, ld ldy (EPI_DTANH_BF16)
   int64_t ldy;
   int tma_epi;           // set by the launcher: output (and y / old output) tiles move by TMA
+  float* colsum;         // dtanh epilogues, TMA path: per 32-row block column sums of the bf16
+  int64_t ldc;           //   output, colsum[(row / 32) * ldc + col] (fused db partials)
 };
 __host__ __device__ constexpr bool epi_f32(int epi) { return epi == EPI_F32 || epi == EPI_F32_ACC; }
 // epilogues that read an [M, N] tile besides the accumulator (y, or the old output)
@@ -451,6 +453,26 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
     }
     fence_proxy_async_smem();
     __syncwarp();
+    if constexpr (uses_y(EPI)) {
+      if (ep.colsum) {  // db partials: lane l sums columns 2l, 2l+1 of the box over its 32 rows, in row order
+        float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+        for (uint32_t r = 0; r < 32; ++r) {
+          const __nv_bfloat162 p2 =
+              *reinterpret_cast<const __nv_bfloat162*>(buf + swz(r, lane >> 2) + ((lane & 3u) << 2));
+          const float2 f = __bfloat1622float2(p2);
+          s0 = __fadd_rn(s0, f.x);
+          s1 = __fadd_rn(s1, f.y);
+        }
+        const int col = c0 + 2 * int(lane);
+        float* dst = ep.colsum + int64_t(r0 / 32) * ep.ldc + col;
+        if (col + 1 < N) {
+          *reinterpret_cast<float2*>(dst) = make_float2(s0, s1);
+        } else if (col < N) {
+          dst[0] = s0;
+        }
+      }
+    }
     if (lane == 0) {
       tma_store_2d(mo, buf, c0, r0);
       bulk_commit();

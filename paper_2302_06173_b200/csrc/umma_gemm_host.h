@@ -95,6 +95,9 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
     if (ok && uses_y(EPI)) ok = make_epi_map(&mi, ep.y, M, N, ep.ldy, 2) == 0;
     if (ok && EPI == EPI_F32_ACC) mi = mo;
     epx.tma_epi = ok ? 1 : 0;
+    // fused column sums exist only in the TMA epilogue (float2 stores: even ldc, 8-byte base)
+    if (ep.colsum && (!ok || !uses_y(EPI) || (ep.ldc & 1) || (reinterpret_cast<uintptr_t>(ep.colsum) & 7)))
+      return static_cast<int>(cudaErrorNotSupported);
   }
   auto kern = umma_gemm_kernel<BN, AMAJ, BMAJ, EPI>;
   static unsigned long long dev_mask = 0;  // the attribute is per device
@@ -133,6 +136,8 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
     if (ok && uses_y(EPI)) ok = make_epi_map(&mi, ep.y, M, N, ep.ldy, 2) == 0;
     if (ok && EPI == EPI_F32_ACC) mi = mo;
     epx.tma_epi = ok ? 1 : 0;
+    if (ep.colsum && (!ok || !uses_y(EPI) || (ep.ldc & 1) || (reinterpret_cast<uintptr_t>(ep.colsum) & 7)))
+      return static_cast<int>(cudaErrorNotSupported);
   }
   auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI>;
   static unsigned long long dev_mask = 0;  // the attribute is per device

@@ -47,6 +47,10 @@ _sig = {
                                        C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p),
                                        C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_void_p]),
+    "rw_stage_backward_ex2": (C.c_int, [C.POINTER(rw_stage_desc), C.c_int64, C.POINTER(C.c_void_p), C.c_void_p,
+                                        C.c_int32, C.c_void_p, C.c_void_p, C.POINTER(C.c_void_p),
+                                        C.POINTER(C.c_void_p), C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_uint64, C.c_void_p]),
     "rw_mse_grad": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p,
                               C.c_void_p, C.c_void_p]),
     "rw_cast_f32_to_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
@@ -154,9 +158,11 @@ class Stage:
     def _scr(self, rows: int):
         if rows not in self._scratch:
             mx = max(self.dims)
+            # fp32 scratch: ceil(rows/32) partial rows, so the dgrad GEMMs form the db sums (ex2)
             self._scratch[rows] = (torch.empty(rows * mx, dtype=torch.bfloat16, device=self.device),
                                    torch.empty(rows * mx, dtype=torch.bfloat16, device=self.device),
-                                   torch.empty(64 * mx, dtype=torch.float32, device=self.device))
+                                   torch.empty(max(64, (rows + 31) // 32) * mx, dtype=torch.float32,
+                                               device=self.device))
         return self._scratch[rows]
 
     # ---- model.cpp entry points ----
@@ -169,16 +175,18 @@ class Stage:
 
     def backward(self, acts: Sequence[torch.Tensor], grad_in: torch.Tensor, grad_out: torch.Tensor | None,
                  accumulate: bool, dw=None, db=None, stream=None, grad_in_is_dz: bool = False,
-                 prev_y: torch.Tensor | None = None) -> None:
+                 prev_y: torch.Tensor | None = None, fuse_db: bool = True) -> None:
         """backward_stage + ordered accumulation into self.grad (or dw/db arrays).
         prev_y / grad_in_is_dz fuse a group-internal stage boundary (see
-        rw_stage_backward_ex): grad_out becomes the previous stage's dz."""
+        rw_stage_backward_ex): grad_out becomes the previous stage's dz.
+        fuse_db: db column sums formed in the dgrad epilogues (rw_stage_backward_ex2)."""
         rows = acts[0].shape[0]
         arr = (C.c_void_p * (self.L + 1))(*[a.data_ptr() for a in acts])
         s0, s1, sf = self._scr(rows)
-        check(LIB.rw_stage_backward_ex(C.byref(self.desc), rows, arr, _p(grad_in), int(grad_in_is_dz),
-                                       _p(grad_out), _p(prev_y), dw or self._dw_c, db or self._db_c,
-                                       int(accumulate), _p(s0), _p(s1), _p(sf), _sh(stream)))
+        check(LIB.rw_stage_backward_ex2(C.byref(self.desc), rows, arr, _p(grad_in), int(grad_in_is_dz),
+                                        _p(grad_out), _p(prev_y), dw or self._dw_c, db or self._db_c,
+                                        int(accumulate), _p(s0), _p(s1), _p(sf), sf.numel() if fuse_db else 0,
+                                        _sh(stream)))
 
     def step(self, hyper: OptimizerHyper, grad: torch.Tensor | None = None, stream=None) -> None:
         """apply_layerwise_updates over this stage (reverse layer order), then

@@ -119,7 +119,8 @@ def test_gemm_engines_agree_bitwise(rows, din, dh, dout):
                 st.forward(acts)
                 g = synth_inputs(5, 1, mb, rows, dout)
                 gout = torch.empty(rows, din, dtype=torch.bfloat16, device="cuda")
-                st.backward(acts, g, gout, accumulate=mb > 0, prev_y=prev)
+                # separate db pass on every engine (the register epilogue cannot fuse it)
+                st.backward(acts, g, gout, accumulate=mb > 0, prev_y=prev, fuse_db=False)
                 outs += [acts[1].clone(), acts[2].clone(), gout]
             torch.cuda.synchronize()
             results.append(outs + [st.grad.clone()])
@@ -128,6 +129,37 @@ def test_gemm_engines_agree_bitwise(rows, din, dh, dout):
     for other in results[1:]:
         for a, b in zip(results[0], other):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("rows", [512, 4096, 200])
+def test_fused_db_matches_separate_column_sums(rows):
+    """db formed in the dgrad epilogue (per-32-row partials of the stored bf16
+    dz, then the partial rows in order) vs the separate column-sum pass over
+    dz: dW, grad_out and the last layer's db are the same bits; the fused
+    layers' db agree to fp32 summation-order error."""
+    st = Stage(2, 128, 512, 256, 3, 9, ADAM)
+    prev = synth_inputs(9, 0, 7, rows, 128)
+    res = []
+    for fuse in (True, False):
+        st.grad.zero_()
+        outs = []
+        for mb in range(2):
+            acts = st.new_acts(rows, synth_inputs(9, 0, mb, rows, 128))
+            st.forward(acts)
+            gout = torch.empty(rows, 128, dtype=torch.bfloat16, device="cuda")
+            st.backward(acts, synth_inputs(9, 1, mb, rows, 256), gout, accumulate=mb > 0, prev_y=prev,
+                        fuse_db=fuse)
+            outs.append(gout)
+        torch.cuda.synchronize()
+        res.append((outs, [st.grad_view(2 * l).clone() for l in range(3)],
+                    [st.grad_view(2 * l + 1).clone() for l in range(3)]))
+    (go_f, dw_f, db_f), (go_u, dw_u, db_u) = res
+    for a, b in zip(go_f + dw_f, go_u + dw_u):
+        assert torch.equal(a, b)
+    assert torch.equal(db_f[2], db_u[2])  # the incoming dz: separate pass in both
+    for l in (0, 1):
+        scale = db_u[l].abs().max().item()
+        assert (db_f[l] - db_u[l]).abs().max().item() <= 1e-5 * scale + 1e-7
 
 
 def _pipeline(kind=ADAM):
