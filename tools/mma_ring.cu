@@ -18,6 +18,8 @@
 //   mode 12: mode 4 + four warps doing tanhf math nonstop (issue-slot competition)
 //   mode 13: mode 4, each step's MMAs read the operands of its own ring stage
 //            (4 x 48 KB of distinct smem, as in the GEMM) instead of one fixed stage
+//   mode 14: mode 13, but the wait for step i+1 is issued after the first two MMAs of
+//            step i (the barrier check overlaps queued MMAs instead of a drained queue)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2302_06173_b200/csrc \
 //        tools/mma_ring.cu -o tools/mma_ring -lcuda
 #include <cuda_bf16.h>
@@ -63,7 +65,42 @@ __global__ void __launch_bounds__(256, 1) ring(int steps, long long* out) {
   tc_fence_after();
   constexpr uint32_t idesc = make_idesc(128, 256, K_MAJOR, K_MAJOR);
   const uint32_t sa = smem_u32(smem), sb = sa + 16384;
-  if (warp == 0) {
+  if (warp == 0 && MODE == 14) {
+    const long long t0 = clock64();
+    for (int i = 0; i < steps; ++i) {
+      const int s = i % S;
+      const uint32_t so = uint32_t(s) * 49152u;
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+          tc_mma(tbase, make_desc(sa + so + k * 32, 16, 1024), make_desc(sb + so + k * 32, 16, 1024), idesc, 1u);
+      }
+      __syncwarp();
+      const int i1 = i + 1;  // next step's stage must be ready before it is issued
+      if (i1 >= S && i1 < steps) {
+        mbar_wait(&full_bar[i1 % S], ((i1 / S) & 1) ^ 1);
+        tc_fence_after();
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 2; k < 4; ++k)
+          tc_mma(tbase, make_desc(sa + so + k * 32, 16, 1024), make_desc(sb + so + k * 32, 16, 1024), idesc, 1u);
+        tc_commit(&empty_bar[s]);
+      }
+      __syncwarp();
+    }
+    __shared__ uint64_t done14;
+    if (lane == 0) {
+      mbar_init(&done14, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      tc_commit(&done14);
+    }
+    __syncwarp();
+    mbar_wait(&done14, 0);
+    const long long t1 = clock64();
+    if (lane == 0) out[blockIdx.x] = t1 - t0;
+    if (lane == 0) mbar_arrive(&end_bar);
+  } else if (warp == 0) {
     const long long t0 = clock64();
     for (int i = 0; i < steps; ++i) {
       const int s = i % S;
@@ -208,5 +245,6 @@ int main() {
   run<11, 4>();
   run<12, 4>();
   run<13, 4>();
+  run<14, 4>();
   return 0;
 }
