@@ -194,6 +194,30 @@ def test_logging_replay_equals_ghost_run_bitwise(kind):
     assert rep.state.markers() == g.markers()
 
 
+def test_logging_replay_equals_ghost_run_config4_shapes():
+    """The same acceptance property at config-4 sizes (stages
+    4096 -> 16384 -> 4096, micro-batch 8 x 2048 = 16384 rows), on a 3-stage
+    pipeline with 2 micro-batches: the middle stage replayed from its logs
+    over 2 iterations equals the ghost run bit for bit (x, m, v, markers)."""
+    h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
+    rows, m = 16384, 2
+    ghost = Pipeline(p=3, dim=4096, hidden=16384, layers=2, rows=rows, micro_batches=m, seed=23, kind=ADAM,
+                     hyper=h)
+    log = BoundaryLog()
+    snap = ghost.stages[1].snapshot()
+    for it in range(2):
+        ghost.run_iteration(log_group=(1, 1), log=log)
+    rep = Stage(1, 4096, 16384, 4096, 2, 23, ADAM)
+    rep.restore(snap)
+    assert replay_group([rep], log, 0, 2, rows, m, 23, h, first=False, last=False, dim=4096) == 2
+    g = ghost.stages[1].state
+    for name in ("x", "m", "v"):
+        assert torch.equal(getattr(rep.state, name).view(torch.int32), getattr(g, name).view(torch.int32)), name
+    assert rep.state.markers() == g.markers()
+    del ghost, rep, log
+    torch.cuda.empty_cache()
+
+
 def test_group_replay_last_stages_bitwise():
     ghost, h = _pipeline()
     log = BoundaryLog(pinned=True)  # logs in pinned host memory
