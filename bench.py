@@ -591,6 +591,68 @@ def config5_sweep(m: int = 8) -> dict:
     return res
 
 
+def logging_bench(records: int = 16, rows: int = 16384, dim: int = 4096) -> dict:
+    """Logging capture path at config-4 boundary size: 16
+    records of [16384, 4096] bf16 (one iteration of 8 micro-batches, activation
+    + gradient) through the native logger (GPU CRC32 + D2H on the logger
+    stream into its pinned slab, SPSC queue, committer thread writing SWFT
+    chunk files).  Reports the producer stream's cost (device time of the
+    producer stream across the log_send calls, host time of the calls) and
+    the capture throughput until flush returns; the GPU CRC32 rate beside."""
+    import shutil
+    import tempfile
+
+    import torch
+
+    from paper_2302_06173_b200.logstore import Logger, crc32_device
+    from paper_2302_06173_b200.replay import synth_inputs
+    root = os.environ.get("RW_LOG_DIR", "/dev/shm" if os.path.isdir("/dev/shm") else "/tmp")
+    nbytes = rows * dim * 2
+    if shutil.disk_usage(root).free < 3 * records * nbytes:
+        return {"skipped": f"not enough space under {root}"}
+    ts = [synth_inputs(3, 0, i, rows, dim) for i in range(4)]
+    d = tempfile.mkdtemp(prefix="rw_log_", dir=root)
+    try:
+        lg = Logger(d, machine=0, chunk_records=8, pinned_bytes=1 << 30)
+        # warm-up record (slab, files, CRC tables)
+        lg.log_send(ts[0], 0, 1, 0, 0, 0)
+        lg.flush()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        for i in range(records):
+            lg.log_send(ts[i % 4], 0, 1, 1, i // 2, i % 2)
+        e1.record()
+        t_call = time.perf_counter() - t0
+        n = lg.flush()
+        t_total = time.perf_counter() - t0
+        torch.cuda.synchronize()
+        producer_ms = e0.elapsed_time(e1)
+        lg.close()
+        # GPU CRC32 throughput on one record (launches only, no host sync in between)
+        import ctypes as C
+        from paper_2302_06173_b200._lib import LIB, check
+        crc32_device(ts[0])
+        out = torch.zeros(1, dtype=torch.int32, device=ts[0].device)
+        sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(10):
+            check(LIB.rw_crc32_device(C.c_void_p(ts[0].data_ptr()), nbytes, C.c_void_p(out.data_ptr()), sh))
+        c1.record()
+        torch.cuda.synchronize()
+        crc_ms = c0.elapsed_time(c1) / 10
+        return dict(records=records, record_bytes=nbytes, committed=int(n) - 1, dir=root,
+                    producer_stream_ms=round(producer_ms, 3), log_send_host_ms_total=round(t_call * 1e3, 2),
+                    capture_s=round(t_total, 3), capture_gbs=round(records * nbytes / t_total / 1e9, 2),
+                    crc32_gbs=round(nbytes / (crc_ms * 1e-3) / 1e9, 1),
+                    note="capture = CRC + D2H into the pinned slab + committer writes of SWFT chunk files "
+                         "until flush (atomic rename); the producer stream only records an event per message")
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+
+
 def checkpoint_bench(sizes, reps: int = 2) -> dict:
     """Global checkpoint write + load of the config-2 Adam state (x, m, v fp32)
     through the native store: pinned pipelined D2H/H2D, GPU CRC32, fsync'd
@@ -921,6 +983,10 @@ def run_b200(args) -> None:
             except torch.cuda.OutOfMemoryError as e:  # pragma: no cover
                 extras["config5_sweep"] = {"error": f"OOM: {e}"}
             torch.cuda.empty_cache()
+            try:
+                extras["logging_capture"] = logging_bench()
+            except Exception as e:  # pragma: no cover - disk space / permissions on the box
+                extras["logging_capture"] = {"error": str(e)[:200]}
             try:
                 extras["checkpoint"] = checkpoint_bench(sizes)
             except Exception as e:  # pragma: no cover - disk space / permissions on the box

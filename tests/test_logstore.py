@@ -86,7 +86,9 @@ def test_logger_roundtrip_and_replay_from_files(tmp_path):
     lg.close()
     assert n == 3 * 4 * 2
     files = sorted(glob.glob(str(tmp_path / "*.swft")))
-    assert len(files) == 5 and not glob.glob(str(tmp_path / "*.tmp"))  # 24 records / 5 per chunk
+    assert not glob.glob(str(tmp_path / "*.tmp"))  # every chunk committed (renamed)
+    per_file = [len(list(logstore.read_chunk(f))) for f in files]  # writer lanes: one open chunk each
+    assert sum(per_file) == 24 and max(per_file) <= 5
     loaded = logstore.load_log_dir(str(tmp_path))
     assert set(loaded.acts) == set(mem.acts) and set(loaded.grads) == set(mem.grads)
     for k in mem.acts:
@@ -116,6 +118,7 @@ def test_logger_does_not_block_producer_stream(tmp_path):
         lg.log_send(t, 0, 1, i, 0, logstore.RW_LOG_ACTIVATION)
     assert lg.flush() == 8
     lg.close()
-    recs = list(logstore.read_chunk(sorted(glob.glob(str(tmp_path / "*.swft")))[0]))
+    recs = [rec for f in sorted(glob.glob(str(tmp_path / "*.swft"))) for rec in logstore.read_chunk(f)]
     assert len(recs) == 8 and all(r.payload_bytes == t.numel() * 2 for r, _ in recs)
+    assert sorted(r.iteration for r, _ in recs) == list(range(8))
     assert all(r.crc32 == logstore.crc32_device(t) for r, _ in recs)

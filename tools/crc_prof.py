@@ -1,0 +1,24 @@
+"""Kernel times of the GPU CRC32 (rw_crc32_device) on a 134 MB record."""
+import ctypes as C
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+from paper_2302_06173_b200._lib import LIB, check  # noqa: E402
+
+x = torch.randint(0, 255, (134217728,), dtype=torch.uint8, device="cuda")
+out = torch.zeros(1, dtype=torch.int32, device="cuda")
+sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+for _ in range(3):
+    check(LIB.rw_crc32_device(C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(out.data_ptr()), sh))
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(5):
+        check(LIB.rw_crc32_device(C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(out.data_ptr()), sh))
+    torch.cuda.synchronize()
+for e in prof.events():
+    if e.device_type.name == "CUDA":
+        print(f"{e.name[:60]:60s} {(e.time_range.end - e.time_range.start):9.1f} us")
