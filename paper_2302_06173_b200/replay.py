@@ -22,6 +22,7 @@ GPU ghost run bit for bit; against the fp64 reference it is tolerance-matched.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Sequence
 
@@ -60,6 +61,9 @@ _sig = {
 for _n, (_r, _a) in _sig.items():
     _f = getattr(LIB, _n)
     _f.restype, _f.argtypes = _r, _a
+
+
+_FUSE_DB = os.environ.get("RW_FUSE_DB", "1") != "0"
 
 
 def _sh(stream=None) -> C.c_void_p:
@@ -175,11 +179,14 @@ class Stage:
 
     def backward(self, acts: Sequence[torch.Tensor], grad_in: torch.Tensor, grad_out: torch.Tensor | None,
                  accumulate: bool, dw=None, db=None, stream=None, grad_in_is_dz: bool = False,
-                 prev_y: torch.Tensor | None = None, fuse_db: bool = True) -> None:
+                 prev_y: torch.Tensor | None = None, fuse_db: bool | None = None) -> None:
         """backward_stage + ordered accumulation into self.grad (or dw/db arrays).
         prev_y / grad_in_is_dz fuse a group-internal stage boundary (see
         rw_stage_backward_ex): grad_out becomes the previous stage's dz.
-        fuse_db: db column sums formed in the dgrad epilogues (rw_stage_backward_ex2)."""
+        fuse_db: db column sums formed in the dgrad epilogues (rw_stage_backward_ex2);
+        None = on unless RW_FUSE_DB=0 (A/B runs)."""
+        if fuse_db is None:
+            fuse_db = _FUSE_DB
         rows = acts[0].shape[0]
         arr = (C.c_void_p * (self.L + 1))(*[a.data_ptr() for a in acts])
         s0, s1, sf = self._scr(rows)
