@@ -126,6 +126,41 @@ def _ncu_traffic(kernel_key: str):
 
 
 # --------------------------------------------------------------- reference arm
+def host_info(n: int = 1 << 26) -> dict:
+    """the CPU the reference runs on -- model, cores, and a
+    STREAM-style triad a = b + s*c over 3 x 512 MB fp64 arrays, split over all
+    cores (numpy releases the GIL), best of 3."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    th = os.cpu_count() or 1
+    a, b, c = np.empty(n), np.full(n, 1.0), np.full(n, 2.0)
+    parts = [(i * n // th, (i + 1) * n // th) for i in range(th)]
+
+    def tri(lo_hi):
+        lo, hi = lo_hi
+        np.multiply(c[lo:hi], 3.0, out=a[lo:hi])
+        np.add(a[lo:hi], b[lo:hi], out=a[lo:hi])
+
+    best = 1e9
+    with ThreadPoolExecutor(th) as ex:
+        for _ in range(3):
+            t0 = time.perf_counter()
+            list(ex.map(tri, parts))
+            best = min(best, time.perf_counter() - t0)
+    # bytes: read c, write a, read a, read b, write a (two numpy passes)
+    return dict(cpu_model=model, nproc=th, triad_gbs=round(5 * 8 * n / best / 1e9, 1),
+                triad_note="a = 3c; a += b over 64M fp64 per array, all cores, 5 x 8 B per element moved")
+
+
 def cpu_reference_undo(seconds_target: float = 1.5, max_elems: int | None = None,
                        threads: int | None = None, steps: int = 1, warmup: int = 0) -> dict:
     """Time the reference optimizer_undo (oracle/_ref, fp64 as shipped) on the
@@ -1024,9 +1059,10 @@ def run_b200(args) -> None:
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            r = cpu_reference_undo(seconds_target=1.0, steps=3, warmup=1)
+            r = cpu_reference_undo(seconds_target=1.0, steps=5, warmup=1)  # median of 5
             cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
             cpu["params_per_s"] = r["params_per_s"]
+            cpu["host"] = host_info()
             # the reference as it runs (one thread) beside the all-core number
             r1 = cpu_reference_undo(seconds_target=0.5, threads=1, steps=1, warmup=0)
             cpu["one_thread"] = dict(value=round(r1["value"], 3), params_per_s=round(r1["params_per_s"], 1),
