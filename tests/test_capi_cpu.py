@@ -181,3 +181,18 @@ def test_logging_worthwhile_matches_restatement():
         assert ours[1] == pytest.approx(exp[1]) and ours[2] == pytest.approx(exp[2])
     # mb=4, hidden=1024, seq=128 -> 524,288 elements per boundary message
     assert planner.boundary_elems(4, 1024, 128) == 524288
+
+
+def test_state_create_rejects_zero_extent_and_overflow():
+    """shape_elements (tensor.cpp:52-56): a zero extent is InvalidShape; a group
+    past the end of the state too -- both checked before any device work."""
+    buf = (C.c_double * 64)()
+    base = (C.addressof(buf) + 15) // 16 * 16
+    out = C.c_void_p()
+    for groups in ([(0, 4), (8, 0)], [(0, 4), (8, 100)]):
+        arr = (rw_group * len(groups))()
+        for i, (o, n) in enumerate(groups):
+            arr[i].offset, arr[i].len = o, n
+        st = LIB.rw_state_create(C.byref(out), 1, C.c_void_p(base), C.c_void_p(base), None, None, None, 32,
+                                 arr, len(groups), 0)
+        assert LIB.rw_status_name(st).decode() == "InvalidShape"

@@ -383,3 +383,28 @@ def test_group_beyond_2_pow_31_elements(restate):
     ux, um, uv, _ = restate.undo(ADAM, h, 4, rx, g0, rm, rv, dtype=np.float32)
     assert np.array_equal(_bits(st.x[idx].cpu().numpy()), _bits(ux))
     assert np.array_equal(_bits(st.m[idx].cpu().numpy()), _bits(um))
+
+
+def test_empty_group_lists_are_noops():
+    """step / undo / host-resident undo over no groups: OK, nothing changes
+    (the batch extension of the one-block call; no launch, no marker write)."""
+    sizes = [1000, 77, 5000]
+    st = DeviceState(sizes, kind=ADAM)
+    seeded_fill_(st.x, 1)
+    seeded_fill_(st.g, 2)
+    seeded_fill_(st.m, 3)
+    seeded_fill_(st.v, 4)
+    st.v.abs_()
+    st.write_markers([(5, 0), (6, 1), (7, 0)])
+    before = {k: getattr(st, k).clone() for k in ("x", "g", "m", "v")}
+    mk = st.markers()
+    h = HYP[ADAM]
+    st.step(h, [])
+    st.undo(h, [])
+    host = {k: getattr(st, k).cpu().pin_memory() for k in ("x", "g", "m", "v")}
+    out = {k: torch.empty_like(host[k]).pin_memory() for k in ("x", "m", "v")}
+    st.undo_from_host(h, host, out, ids=[])
+    torch.cuda.synchronize()
+    assert st.markers() == mk
+    for k, t in before.items():
+        assert torch.equal(getattr(st, k), t), k
