@@ -25,15 +25,33 @@ using bf16 = __nv_bfloat16;
 constexpr int kBN = 256;
 constexpr int kPairDefault = 0;
 
+__device__ __forceinline__ bf16 dtanh1(bf16 g, bf16 y) {
+  // dz = dL/dy * (1 - y^2)   (model.cpp:185-192)
+  const float yv = __bfloat162float(y);
+  return __float2bfloat16_rn(__fmul_rn(__bfloat162float(g), __fsub_rn(1.f, __fmul_rn(yv, yv))));
+}
+// 8 elements per thread per step (16-byte loads / store) when the pointers allow
 __global__ void dtanh_first_kernel(const bf16* __restrict__ g, const bf16* __restrict__ y,
                                    bf16* __restrict__ dz, uint64_t n) {
-  // dz = dL/dy * (1 - y^2)   (model.cpp:185-192)
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const float yv = __bfloat162float(y[i]);
-    const float d = __fmul_rn(__bfloat162float(g[i]), __fsub_rn(1.f, __fmul_rn(yv, yv)));
-    dz[i] = __float2bfloat16_rn(d);
+  const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x, nt = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(g) | reinterpret_cast<uintptr_t>(y) | reinterpret_cast<uintptr_t>(dz)) & 15u) ==
+      0) {
+    const uint64_t n8 = n / 8;
+    for (uint64_t i = tid; i < n8; i += nt) {
+      const uint4 gv = __ldg(reinterpret_cast<const uint4*>(g) + i);
+      const uint4 yv = __ldg(reinterpret_cast<const uint4*>(y) + i);
+      const bf16* gp = reinterpret_cast<const bf16*>(&gv);
+      const bf16* yp = reinterpret_cast<const bf16*>(&yv);
+      uint4 o;
+      bf16* op = reinterpret_cast<bf16*>(&o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) op[k] = dtanh1(gp[k], yp[k]);
+      reinterpret_cast<uint4*>(dz)[i] = o;
+    }
+    done = n8 * 8;
   }
+  for (uint64_t i = done + tid; i < n; i += nt) dz[i] = dtanh1(g[i], y[i]);
 }
 
 // db[c] (+)= sum_r dz[r, c]: fixed two-level order (row splits summed in order)
@@ -57,10 +75,29 @@ __global__ void colsum_final_kernel(const float* __restrict__ part, int64_t nspl
   db[c] = accumulate ? __fadd_rn(db[c], acc) : acc;
 }
 
+// 8 elements per thread per step (two 16-byte loads, one 16-byte store) when
+// both pointers allow it; the scalar loop covers the rest
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out, uint64_t n) {
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
-       i += uint64_t(gridDim.x) * blockDim.x)
-    out[i] = __float2bfloat16_rn(in[i]);
+  const uint64_t tid = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x, nt = uint64_t(gridDim.x) * blockDim.x;
+  uint64_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15u) == 0) {
+    const uint64_t n8 = n / 8;
+    const float4* i4 = reinterpret_cast<const float4*>(in);
+    uint4* o4 = reinterpret_cast<uint4*>(out);
+    for (uint64_t i = tid; i < n8; i += nt) {
+      const float4 a = __ldg(i4 + 2 * i), b = __ldg(i4 + 2 * i + 1);
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x, a.y), h1 = __floats2bfloat162_rn(a.z, a.w);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(b.x, b.y), h3 = __floats2bfloat162_rn(b.z, b.w);
+      uint4 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&h0);
+      pk.y = *reinterpret_cast<uint32_t*>(&h1);
+      pk.z = *reinterpret_cast<uint32_t*>(&h2);
+      pk.w = *reinterpret_cast<uint32_t*>(&h3);
+      o4[i] = pk;
+    }
+    done = n8 * 8;
+  }
+  for (uint64_t i = done + tid; i < n; i += nt) out[i] = __float2bfloat16_rn(in[i]);
 }
 
 // mse_loss (model.cpp:174-188): grad = 2/(n*mbs) * (pred - target); the
