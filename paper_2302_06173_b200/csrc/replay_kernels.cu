@@ -56,15 +56,31 @@ __global__ void dtanh_first_kernel(const bf16* __restrict__ g, const bf16* __res
 
 // db[c] (+)= sum_r dz[r, c]: fixed two-level order (row splits summed in order)
 constexpr int kColSplit = 64;
+// one thread per column pair (4-byte loads: 128 contiguous bytes per warp and
+// row), rows of split s summed in order
 __global__ void colsum_partial_kernel(const bf16* __restrict__ dz, int64_t rows, int64_t cols,
                                       float* __restrict__ part) {
-  const int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  const int64_t c = 2 * (blockIdx.x * int64_t(blockDim.x) + threadIdx.x);
   const int s = blockIdx.y;
   if (c >= cols) return;
   const int64_t r0 = rows * s / kColSplit, r1 = rows * (s + 1) / kColSplit;
-  float acc = 0.f;
-  for (int64_t r = r0; r < r1; ++r) acc = __fadd_rn(acc, __bfloat162float(dz[r * cols + c]));
-  part[int64_t(s) * cols + c] = acc;
+  float a0 = 0.f, a1 = 0.f;
+  if (c + 1 < cols && (cols & 1) == 0) {
+    for (int64_t r = r0; r < r1; ++r) {
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dz + r * cols + c));
+      a0 = __fadd_rn(a0, f.x);
+      a1 = __fadd_rn(a1, f.y);
+    }
+    part[int64_t(s) * cols + c] = a0;
+    part[int64_t(s) * cols + c + 1] = a1;
+  } else {
+    for (int64_t r = r0; r < r1; ++r) {
+      a0 = __fadd_rn(a0, __bfloat162float(dz[r * cols + c]));
+      if (c + 1 < cols) a1 = __fadd_rn(a1, __bfloat162float(dz[r * cols + c + 1]));
+    }
+    part[int64_t(s) * cols + c] = a0;
+    if (c + 1 < cols) part[int64_t(s) * cols + c + 1] = a1;
+  }
 }
 __global__ void colsum_final_kernel(const float* __restrict__ part, int64_t nsplit, int64_t cols,
                                     float* __restrict__ db, int accumulate) {
@@ -253,7 +269,7 @@ int replay_dtanh_first(const void* g, const void* y, void* dz, uint64_t n, void*
 int replay_colsum(const void* dz, int64_t rows, int64_t cols, float* db, float* scratch, int accumulate,
                   void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
-  dim3 g(unsigned((cols + 127) / 128), kColSplit);
+  dim3 g(unsigned((cols + 255) / 256), kColSplit);  // 128 threads x 2 columns
   colsum_partial_kernel<<<g, 128, 0, st>>>(static_cast<const bf16*>(dz), rows, cols, scratch);
   colsum_final_kernel<<<unsigned((cols + 127) / 128), 128, 0, st>>>(scratch, kColSplit, cols, db, accumulate);
   return static_cast<int>(cudaGetLastError());
