@@ -148,6 +148,27 @@ def _export(t: torch.Tensor) -> tuple[bytes, int]:
     return bytes(h), off.value
 
 
+def _allgather_exports(tensors: Sequence[torch.Tensor], group=None) -> list[list[tuple[bytes, int]]]:
+    """Every rank's CUDA-IPC exports of `tensors` (the same count on every
+    rank): the 64-byte handles and offsets travel as one small byte tensor in
+    a single all_gather on the group's backend (~0.05 ms over NCCL) instead
+    of a pickled all_gather_object (~1 ms)."""
+    world = dist.get_world_size(group)
+    k = len(tensors)
+    rec = torch.empty(k, 72, dtype=torch.uint8)
+    for i, t in enumerate(tensors):
+        hb, off = _export(t)
+        rec[i, :64] = torch.frombuffer(bytearray(hb), dtype=torch.uint8)
+        rec[i, 64:] = torch.frombuffer(bytearray(int(off).to_bytes(8, "little")), dtype=torch.uint8)
+    dev = tensors[0].device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    mine = rec.to(dev)
+    allr = torch.empty(world * k, 72, dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(allr, mine, group=group)
+    flat = allr.cpu().numpy()
+    return [[(flat[r * k + i, :64].tobytes(), int.from_bytes(flat[r * k + i, 64:].tobytes(), "little"))
+             for i in range(k)] for r in range(world)]
+
+
 def recover_replication_fused(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False,
                               group=None, stream=None) -> int:
     """apply_undo + recover_replication in ONE kernel on the survivor `src`:
@@ -431,9 +452,8 @@ def recover_replication_chain(state, hyper, plan: ResolvePlan, src: int, include
     # handles are exchanged on every call (the peers' buffers may have moved);
     # the mappings themselves are cached by handle in _PEER_MAPS
     counters = torch.zeros(n_pieces, dtype=torch.int64, device=state.device)
-    mine = dict(bufs={n: _export(getattr(state, n)) for n in names}, counters=_export(counters))
-    allh: list = [None] * world
-    dist.all_gather_object(allh, mine, group=group)
+    ex = _allgather_exports([getattr(state, n) for n in names] + [counters], group)
+    allh = [dict(bufs=dict(zip(names, e[:-1])), counters=e[-1]) for e in ex]
     chain = [src] + [r for r in range(world) if r != src]
     pos = chain.index(rank)
     nxt = None
