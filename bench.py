@@ -672,12 +672,15 @@ def logging_bench(records: int = 16, rows: int = 16384, dim: int = 4096) -> dict
         out = torch.zeros(1, dtype=torch.int32, device=ts[0].device)
         sh = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        c0.record()
-        for _ in range(10):
-            check(LIB.rw_crc32_device(C.c_void_p(ts[0].data_ptr()), nbytes, C.c_void_p(out.data_ptr()), sh))
-        c1.record()
-        torch.cuda.synchronize()
-        crc_ms = c0.elapsed_time(c1) / 10
+        windows = []
+        for _ in range(4):  # first window warms clocks and the allocator; median of the rest
+            c0.record()
+            for _ in range(10):
+                check(LIB.rw_crc32_device(C.c_void_p(ts[0].data_ptr()), nbytes, C.c_void_p(out.data_ptr()), sh))
+            c1.record()
+            torch.cuda.synchronize()
+            windows.append(c0.elapsed_time(c1) / 10)
+        crc_ms = statistics.median(windows[1:])
         return dict(records=records, record_bytes=nbytes, committed=int(n) - 1, dir=root,
                     producer_stream_ms=round(producer_ms, 3), log_send_host_ms_total=round(t_call * 1e3, 2),
                     capture_s=round(t_total, 3), capture_gbs=round(records * nbytes / t_total / 1e9, 2),
