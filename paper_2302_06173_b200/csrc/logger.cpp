@@ -299,6 +299,20 @@ extern "C" {
 int rw_crc32_device(const void* data, uint64_t n, uint32_t* out_dev, void* stream) {
   rwb::DeviceScope dev_scope(rwb::DeviceScope::device_of(data));
   if ((!data && n) || !out_dev) return lfail(RW_INVALID_ARGUMENT, "null argument");
+  // the scratch comes from the device's default stream-ordered pool; keep a
+  // few MB of it cached (release threshold) so a call does not map and unmap
+  // memory each time (the default threshold of 0 returns it at every sync)
+  static unsigned long long pool_mask = 0;
+  if (rwb::first_on_device(pool_mask)) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = 64ull << 20;
+      uint64_t cur = 0;
+      if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < keep)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   uint32_t* scratch = nullptr;
   LCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), rwb::crc32_scratch_words(n) * 4,
                         static_cast<cudaStream_t>(stream)));

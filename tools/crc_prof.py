@@ -22,3 +22,17 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
 for e in prof.events():
     if e.device_type.name == "CUDA":
         print(f"{e.name[:60]:60s} {(e.time_range.end - e.time_range.start):9.1f} us")
+
+# event-timed windows of 10 calls (as bench.logging_bench) and host time per call
+import time  # noqa: E402
+for w in range(4):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(10):
+        check(LIB.rw_crc32_device(C.c_void_p(x.data_ptr()), x.numel(), C.c_void_p(out.data_ptr()), sh))
+    e1.record()
+    th = (time.perf_counter() - t0) / 10 * 1e3
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    print(f"window {w}: {ms:.3f} ms per call on the GPU timeline = {x.numel() / ms / 1e6:.0f} GB/s, host {th:.3f} ms per call")
