@@ -60,10 +60,12 @@ def crc32_device(t: torch.Tensor, stream=None) -> int:
 
 
 class Logger:
-    """Upstream-backup logger of one machine."""
+    """Upstream-backup logger of one machine.  pinned_bytes is
+    the host staging slab: a few boundary records (a config-4 record is 134 MB)
+    so log_send rarely waits for the writer lanes."""
 
     def __init__(self, directory: str, machine: int, chunk_records: int = 64,
-                 pinned_bytes: int = 256 << 20, device: int | None = None):
+                 pinned_bytes: int = 1 << 30, device: int | None = None):
         os.makedirs(directory, exist_ok=True)
         self.dir = directory
         self._h = _vp()
