@@ -16,9 +16,9 @@
  *    exact rewind::Error the reference would have raised; 100+ are
  *    B200-side failures (CUDA error, bad argument) with no reference twin;
  *  - guards are checked in the reference's order BEFORE any mutation
- *    (optim.cpp:340-348 for step, :367-370 plus the per-kind hyper checks for
+ *    (optim.cpp:262-270 for step, :289-292 plus the per-kind hyper checks for
  *    undo); NumericalError is detected in-kernel (fused check_finite,
- *    optim.cpp:361-363/:382-384) and reported after mutation by
+ *    optim.cpp:283-285/:304-306) and reported after mutation by
  *    rw_state_check(), exactly like the reference raises after mutating;
  *  - thread-safe across distinct rw_state objects; one rw_state must not be
  *    used from two host threads at once (one owner per block).
@@ -105,11 +105,11 @@ const char* rw_last_error_message(void); /* thread-local, message of the last fa
 const char* rw_status_name(int status);  /* err_name (errors.cpp:8-31) for 1..19 */
 int rw_device_count(void);
 
-/* invertibility_check(OptimizerKind), optim.hpp:32 / optim.cpp:113-126 */
+/* invertibility_check(OptimizerKind), optim.hpp:32 / optim.cpp:35-48 */
 int rw_invertibility_check(int32_t kind);
-/* OptimizerHyper::validate, optim.cpp:137-149 */
+/* OptimizerHyper::validate, optim.cpp:59-71 */
 int rw_hyper_validate(const rw_hyper* h);
-/* OptimizerHyper::lr_at, optim.cpp:128-135 */
+/* OptimizerHyper::lr_at, optim.cpp:50-57 */
 int rw_lr_at(const rw_hyper* h, uint64_t t, double* out);
 
 /* ---- flat optimizer state (the device form of a set of ParamBlocks) ----
@@ -123,6 +123,15 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
                     int32_t device);
 void rw_state_destroy(rw_state* s);
 uint32_t rw_state_num_groups(const rw_state* s);
+/* Behaviour flags of a state (default 0).
+ * RW_STATE_LAMB_SEQUENTIAL_NORMS: the LAMB step forms ||x|| and ||update|| in
+ *   the reference's left-to-right order (optim.cpp:199-208, one thread per
+ *   group) instead of the parallel fixed-order tree, so the trust ratio -- and
+ *   therefore x and the saved scalar -- equal rewind::optimizer_step's bit for
+ *   bit (fp64).  O(n) per group on one thread: meant for parity / drop-in use
+ *   (the host-block entry points set it); the default tree agrees to ~1e-15. */
+enum { RW_STATE_LAMB_SEQUENTIAL_NORMS = 1 };
+int rw_state_set_flags(rw_state* s, uint32_t flags);
 /* Copy the device marker table to `out` (n_groups records).  Synchronises
  * `stream`.  The device table is authoritative after a crash-injected step. */
 int rw_state_read_groups(rw_state* s, rw_group* out, void* stream);
@@ -137,8 +146,8 @@ int rw_clear_updated(rw_state* s, const uint32_t* group_ids, uint32_t n, void* s
 /* Device pointers of the flat buffers (for collectives / copies). */
 void* rw_state_ptr(rw_state* s, int which /*0 x,1 g,2 m,3 v,4 vmax*/);
 
-/* LAMB saved scalars (ParamBlock::saved_scalars, optim.hpp / optim.cpp:294,
- * :319).  Each group keeps the last RW_LAMB_TRUST_DEPTH trust ratios on the
+/* LAMB saved scalars (ParamBlock::saved_scalars, optim.hpp / optim.cpp:216,
+ * :241).  Each group keeps the last RW_LAMB_TRUST_DEPTH trust ratios on the
  * device (a step pushes, an undo pops; older entries fall off, so at most
  * RW_LAMB_TRUST_DEPTH consecutive undos find their ratio).  read copies the
  * stack bottom->top into out (at most cap) and its depth into *count
@@ -150,10 +159,10 @@ int rw_state_saved_scalars(rw_state* s, uint32_t group, double* out, uint32_t ca
 int rw_state_set_saved_scalars(rw_state* s, uint32_t group, const double* in, uint32_t count, void* stream);
 
 /* optimizer_step(ParamBlock&, const Tensor& grad, const OptimizerHyper&),
- * optim.hpp:71-72 / optim.cpp:338-364 — batched over `n` groups given in
+ * optim.hpp:71-72 / optim.cpp:260-286 — batched over `n` groups given in
  * UPDATE ORDER (apply_layerwise_updates: reverse layer order).
  * grad: flat device gradient in the same layout (NULL = g already holds it);
- * the kernel caches it into g (optim.cpp:349) in the same pass.
+ * the kernel caches it into g (optim.cpp:271) in the same pass.
  * stop_after: crash injection MidUpdate(k): only the first
  * min(n, stop_after) groups in update order are stepped; UINT32_MAX = all.
  * Guards for ALL n groups are checked before anything is launched. */
@@ -161,12 +170,13 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* group_ids,
                       const void* grad, uint32_t stop_after, void* stream);
 
 /* optimizer_undo(ParamBlock&, const OptimizerHyper&), optim.hpp:76 /
- * optim.cpp:366-385 — batched over `n` groups.
+ * optim.cpp:288-307 — batched over `n` groups.
  * LAMB (step and undo): the step runs a per-group norm pass (m, v, ||x||,
  * ||update|| in fp64 with a fixed reduction order) and then the fused x pass
  * with scaled = eta * trust; the undo reads the saved ratio (one D2H read) and
  * is one fused elementwise pass.  The trust ratio differs from the reference's
- * sequential sum in the last bits (documented tolerance); m, v are bit-exact. */
+ * sequential sum in the last bits (documented tolerance; m, v are bit-exact)
+ * unless the state has RW_STATE_LAMB_SEQUENTIAL_NORMS. */
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,
                       void* stream);
 
@@ -211,7 +221,7 @@ int rw_undo_and_push(rw_state* s, const rw_hyper* h, const uint32_t* undo_ids, u
                      void* peer_x, void* peer_g, void* peer_m, void* peer_v, void* stream);
 
 /* ---- host-buffer entry points: ONE reference ParamBlock held in host memory ----
- * Exactly optimizer_step / optimizer_undo (optim.cpp:338-385) on a block whose
+ * Exactly optimizer_step / optimizer_undo (optim.cpp:260-307) on a block whose
  * x, g, m, v (and AMSGrad vmax) live in host memory: the library stages them
  * through device memory it owns (per calling thread), runs the fused kernel,
  * copies the results back and reports NumericalError like the reference
@@ -223,8 +233,8 @@ int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* 
 int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n,
                        uint64_t* t, uint32_t* updated, const rw_hyper* h);
 /* LAMB on a host ParamBlock: the block's saved_scalars stack stays with the
- * caller.  step returns the ratio step_lamb pushes (optim.cpp:294) in
- * *trust_out; undo takes the stack top (the caller pops it on RW_OK, :319).
+ * caller.  step returns the ratio step_lamb pushes (optim.cpp:216) in
+ * *trust_out; undo takes the stack top (the caller pops it on RW_OK, :241).
  * rw_host_block_step/undo refuse RW_LAMB (they have no saved-scalar slot). */
 int rw_host_block_lamb_step(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
                             uint32_t* updated, const void* grad, const rw_hyper* h, double* trust_out);
@@ -251,7 +261,9 @@ typedef struct rw_resolve_summary {
  * buffer (NULL = none ready).  Two phases: t_floor = UINT64_MAX gives the
  * local t_min/t_max (all-reduce them MIN/MAX); then call again with
  * t_floor = the global t_min to get costs/blocks relative to it (all-reduce
- * the remaining fields with MAX). */
+ * the remaining fields with MAX).  n == 0 (a replacement holding no state)
+ * yields t_min = UINT64_MAX and t_max = 0, the identities of MIN / MAX, so it
+ * can join the all-reduces without moving the consensus. */
 int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad_ready,
                          const rw_hyper* h, uint64_t t_floor, rw_resolve_summary* out);
 /* Given the all-reduced summary (t_min MIN, t_max MAX, the rest MAX), pick a
@@ -381,6 +393,10 @@ int rw_logger_log(rw_logger* lg, const rw_log_record* rec, const void* dev_paylo
 /* flush_logs: drain the queue, commit the partial chunk. */
 int rw_logger_flush(rw_logger* lg, uint64_t* records_committed);
 int rw_logger_destroy(rw_logger* lg);
+/* The logger's copy stream (cudaStream_t): a caller whose device memory
+ * allocator is stream-ordered marks each logged payload as used on it, so the
+ * memory is recycled only after the D2H has read it (no keep-alive list). */
+void* rw_logger_stream(rw_logger* lg);
 
 typedef struct rw_log_reader rw_log_reader;
 int rw_log_open(rw_log_reader** out, const char* path, uint32_t* machine);

@@ -20,8 +20,11 @@
 //
 // Without the macro, rewind_b200::Error (same Err numbering) is thrown.
 // State stays fp64 as in the reference, so results are bit-identical to
-// rewind::optimizer_step / optimizer_undo (the kernel evaluates the same
-// IEEE operation sequence; tests/cpp/dropin_test.cpp checks it).
+// rewind::optimizer_step / optimizer_undo for every optimizer (the kernel
+// evaluates the same IEEE operation sequence; for LAMB the host-block path
+// forms the two norms in the reference's left-to-right order, so the trust
+// ratio pushed to saved_scalars is the reference's too);
+// tests/cpp/dropin_test.cpp checks it.
 #pragma once
 
 #include <cstdint>
@@ -108,8 +111,8 @@ Invertibility invertibility_check(Kind kind) {
   return static_cast<Invertibility>(rw_invertibility_check(static_cast<int32_t>(kind)));
 }
 
-// optimizer_step(ParamBlock&, const Tensor& grad, const OptimizerHyper&), optim.cpp:338-364.
-// ShapeMismatch is checked first (:340), then the C ABI applies the same
+// optimizer_step(ParamBlock&, const Tensor& grad, const OptimizerHyper&), optim.cpp:260-286.
+// ShapeMismatch is checked first (:262), then the C ABI applies the same
 // guards in the same order and runs the fused kernel on the block.
 template <class Block, class Tensor, class Hyper>
 void optimizer_step(Block& block, const Tensor& grad, const Hyper& hyper) {
@@ -125,14 +128,14 @@ void optimizer_step(Block& block, const Tensor& grad, const Hyper& hyper) {
   if (block.g.data.size() != n) block.g.data.assign(n, 0.0);
   if (block.m.data.size() != n) block.m.data.assign(n, 0.0);
   if (block.v.data.size() != n) block.v.data.assign(n, 0.0);
-  if (h.c.kind == RW_AMSGRAD && block.vmax.data.size() != n) {  // optim.cpp:323
+  if (h.c.kind == RW_AMSGRAD && block.vmax.data.size() != n) {  // optim.cpp:245
     block.vmax.shape = block.x.shape;
     block.vmax.data.assign(n, 0.0);
   }
   block.g.shape = block.x.shape;
   uint64_t t = block.t;
   uint32_t upd = block.updated ? 1u : 0u;
-  if (h.c.kind == RW_LAMB) {  // step_lamb pushes its trust ratio (optim.cpp:294)
+  if (h.c.kind == RW_LAMB) {  // step_lamb pushes its trust ratio (optim.cpp:216)
     double trust = 0.0;
     const int sl = rw_host_block_lamb_step(RW_F64, block.x.data.data(), block.g.data.data(), block.m.data.data(),
                                            block.v.data.data(), n, &t, &upd, grad.data.data(), &h.c, &trust);
@@ -151,14 +154,14 @@ void optimizer_step(Block& block, const Tensor& grad, const Hyper& hyper) {
   detail::check(st);
 }
 
-// optimizer_undo(ParamBlock&, const OptimizerHyper&), optim.cpp:366-385.
+// optimizer_undo(ParamBlock&, const OptimizerHyper&), optim.cpp:288-307.
 template <class Block, class Hyper>
 void optimizer_undo(Block& block, const Hyper& hyper) {
   detail::HyperC<Hyper> h(hyper);
   const uint64_t n = block.x.data.size();
   uint64_t t = block.t;
   uint32_t upd = block.updated ? 1u : 0u;
-  if (h.c.kind == RW_LAMB) {  // undo_lamb consumes the top ratio (optim.cpp:305-319)
+  if (h.c.kind == RW_LAMB) {  // undo_lamb consumes the top ratio (optim.cpp:227-241)
     const bool have = !block.saved_scalars.empty();
     const int sl = rw_host_block_lamb_undo(RW_F64, block.x.data.data(), detail::ptr_or_null(block.g),
                                            detail::ptr_or_null(block.m), detail::ptr_or_null(block.v), n, &t, &upd,

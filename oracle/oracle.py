@@ -281,10 +281,6 @@ class Restate:
         L.oracle_undo_lamb_f64.argtypes = [P(or_scalars), C.c_double, _dp, _dp, _dp, _dp, sz]
         L.oracle_derive_seed.restype = u64
         L.oracle_derive_seed.argtypes = [u64, P(u64), C.c_int]
-        L.oracle_check_const_div_f32.restype = u64
-        L.oracle_check_const_div_f32.argtypes = [C.c_float, C.c_float, C.c_float]
-        L.oracle_check_const_div_f64_sampled.restype = u64
-        L.oracle_check_const_div_f64_sampled.argtypes = [C.c_double, u64, u64]
 
     @staticmethod
     def hyper(h) -> or_hyper:

@@ -7,7 +7,7 @@
 #include <math.h>
 #include <string.h>
 
-/* optim.cpp:128-135 (last breakpoint with t >= from wins). */
+/* optim.cpp:50-57 (last breakpoint with t >= from wins). */
 double oracle_lr_at(const or_hyper* h, uint64_t t) {
   double out = h->lr;
   for (int i = 0; i < h->n_lr_table; ++i)
@@ -17,8 +17,8 @@ double oracle_lr_at(const or_hyper* h, uint64_t t) {
 
 int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars* s) {
   memset(s, 0, sizeof(*s));
-  /* step uses lr_at(t+1) and bias_correction(t+1) (optim.cpp:350, :210);
-   * undo uses lr_at(t) and bias_correction(t) (optim.cpp:371, :225). */
+  /* step uses lr_at(t+1) and bias_correction(t+1) (optim.cpp:272, :132);
+   * undo uses lr_at(t) and bias_correction(t) (optim.cpp:293, :147). */
   uint64_t tt = is_undo ? t_before : t_before + 1;
   s->eta = oracle_lr_at(h, tt);
   if (!(s->eta > 0.0)) return 1 + 17; /* Err::InvalidConfig */
@@ -50,16 +50,16 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
     int fin = 0;                                                                           \
     for (size_t i = 0; i < n; ++i) {                                                       \
       switch (kind) {                                                                      \
-        case OR_SGD: /* optim.cpp:177-181 */                                               \
+        case OR_SGD: /* optim.cpp:99-103 */                                               \
           x[i] = x[i] - eta * (g[i] + wd * x[i]);                                          \
           break;                                                                           \
-        case OR_SGDM: { /* optim.cpp:191-197 */                                            \
+        case OR_SGDM: { /* optim.cpp:113-119 */                                            \
           T gd = g[i] + wd * x[i];                                                         \
           m[i] = mu * m[i] + omd * gd;                                                     \
           x[i] = x[i] - eta * m[i];                                                        \
           break;                                                                           \
         }                                                                                  \
-        case OR_ADAM: { /* optim.cpp:209-219 */                                            \
+        case OR_ADAM: { /* optim.cpp:131-141 */                                            \
           T gd = g[i] + wd * x[i];                                                         \
           m[i] = b1 * m[i] + omb1 * gd;                                                    \
           v[i] = b2 * v[i] + omb2 * gd * gd;                                               \
@@ -68,7 +68,7 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
           x[i] = x[i] - eta * mhat / (SQRT(vhat) + eps);                                   \
           break;                                                                           \
         }                                                                                  \
-        case OR_ADAMW: { /* optim.cpp:238-249 */                                           \
+        case OR_ADAMW: { /* optim.cpp:160-171 */                                           \
           T gd = g[i];                                                                     \
           m[i] = b1 * m[i] + omb1 * gd;                                                    \
           v[i] = b2 * v[i] + omb2 * gd * gd;                                               \
@@ -93,17 +93,17 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
     int fin = 0;                                                                           \
     for (size_t i = 0; i < n; ++i) {                                                       \
       switch (kind) {                                                                      \
-        case OR_SGD: /* optim.cpp:183-189 */                                               \
+        case OR_SGD: /* optim.cpp:105-111 */                                               \
           x[i] = (x[i] + eta * g[i]) / denom;                                              \
           break;                                                                           \
-        case OR_SGDM: { /* optim.cpp:199-207 */                                            \
+        case OR_SGDM: { /* optim.cpp:121-129 */                                            \
           T xt = x[i] + eta * m[i];                                                        \
           T gd = g[i] + wd * xt;                                                           \
           m[i] = (m[i] - omd * gd) / mu;                                                   \
           x[i] = xt;                                                                       \
           break;                                                                           \
         }                                                                                  \
-        case OR_ADAM: { /* optim.cpp:221-235 */                                            \
+        case OR_ADAM: { /* optim.cpp:143-157 */                                            \
           T mhat = m[i] / c1;                                                              \
           T vhat = v[i] / c2;                                                              \
           T xt = x[i] + eta * mhat / (SQRT(vhat) + eps);                                   \
@@ -113,7 +113,7 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
           x[i] = xt;                                                                       \
           break;                                                                           \
         }                                                                                  \
-        case OR_ADAMW: { /* optim.cpp:251-267 */                                           \
+        case OR_ADAMW: { /* optim.cpp:173-189 */                                           \
           T mhat = m[i] / c1;                                                              \
           T vhat = v[i] / c2;                                                              \
           T xt = (x[i] + eta * mhat / (SQRT(vhat) + eps)) / denom;                         \
@@ -136,7 +136,7 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
     const T b1 = (T)S->b1, b2 = (T)S->b2, omb1 = (T)S->one_m_b1;                          \
     const T omb2 = (T)S->one_m_b2, eps = (T)S->eps;                                       \
     int fin = 0;                                                                           \
-    for (size_t i = 0; i < n; ++i) { /* optim.cpp:322-334 */                               \
+    for (size_t i = 0; i < n; ++i) { /* optim.cpp:244-256 */                               \
       T gd = g[i] + wd * x[i];                                                             \
       m[i] = b1 * m[i] + omb1 * gd;                                                        \
       v[i] = b2 * v[i] + omb2 * gd * gd;                                                   \
@@ -158,7 +158,7 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
 DEFINE_LOOPS(double, f64, sqrt)
 DEFINE_LOOPS(float, f32, sqrtf)
 
-/* LAMB step, optim.cpp:273-295 (fp64 only: the trust-ratio norms are
+/* LAMB step, optim.cpp:195-217 (fp64 only: the trust-ratio norms are
  * sequential left-to-right sums). */
 int oracle_step_lamb_f64(const or_scalars* S, double* x, const double* g, double* m, double* v,
                          size_t n, double* trust_out) {
@@ -189,7 +189,7 @@ int oracle_step_lamb_f64(const or_scalars* S, double* x, const double* g, double
   return fin;
 }
 
-/* LAMB undo, optim.cpp:297-320. */
+/* LAMB undo, optim.cpp:219-242. */
 int oracle_undo_lamb_f64(const or_scalars* S, double trust, double* x, const double* g, double* m,
                          double* v, size_t n) {
   double scaled = S->eta * trust;
@@ -232,40 +232,4 @@ void oracle_seeded_fill_f64(uint64_t seed, size_t n, double* out) {
 }
 void oracle_seeded_fill_f32(uint64_t seed, size_t n, float* out) {
   for (size_t i = 0; i < n; ++i) out[i] = (float)((unit_at(seed, i) * 2.0 - 1.0) * 0.1);
-}
-
-/* See restate.h.  a runs over every float in [lo_mant, hi_mant) (a binade). */
-uint64_t oracle_check_const_div_f32(float b, float lo, float hi) {
-  const float r = 1.0f / b; /* RN(1/b) */
-  uint64_t bad = 0;
-  union { float f; uint32_t u; } a, e;
-  a.f = lo;
-  e.f = hi;
-  for (uint32_t u = a.u; u < e.u; ++u) {
-    union { float f; uint32_t u; } av;
-    av.u = u;
-    float q = av.f * r;
-    float rem = fmaf(-q, b, av.f);
-    float q1 = fmaf(rem, r, q);
-    float ref = av.f / b;
-    if (q1 != ref) ++bad;
-  }
-  return bad;
-}
-
-uint64_t oracle_check_const_div_f64_sampled(double b, uint64_t samples, uint64_t seed) {
-  const double r = 1.0 / b;
-  uint64_t bad = 0;
-  for (uint64_t i = 0; i < samples; ++i) {
-    uint64_t bits = oracle_mix64(seed ^ (i * 0x9E3779B97F4A7C15ull + 1));
-    /* mantissa random, exponent fixed to [1,2) */
-    bits = (bits & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull;
-    union { double d; uint64_t u; } a;
-    a.u = bits;
-    double q = a.d * r;
-    double rem = fma(-q, b, a.d);
-    double q1 = fma(rem, r, q);
-    if (q1 != a.d / b) ++bad;
-  }
-  return bad;
 }

@@ -32,8 +32,8 @@ typedef struct {
 
 /* Every per-call scalar the loops use, derived in double as optim.cpp does. */
 typedef struct {
-  double eta;         /* lr_at(t+1) for step (optim.cpp:350), lr_at(t) for undo (:371) */
-  double c1, c2;      /* bias_correction (optim.cpp:172-175) at t+1 (step) / t (undo) */
+  double eta;         /* lr_at(t+1) for step (optim.cpp:272), lr_at(t) for undo (:293) */
+  double c1, c2;      /* bias_correction (optim.cpp:94-97) at t+1 (step) / t (undo) */
   double wd, mu, one_m_damp, b1, b2, one_m_b1, one_m_b2, eps;
   double denom;       /* 1 - eta*wd (undo_sgd :184, undo_adamw :255) */
 } or_scalars;
@@ -43,17 +43,17 @@ int oracle_scalars(const or_hyper* h, uint64_t t_before, int is_undo, or_scalars
 double oracle_lr_at(const or_hyper* h, uint64_t t);
 
 /* Element loops.  Return 1 if any of x, m, v is non-finite afterwards
- * (check_finite at optim.cpp:361-363 / :382-384), else 0. */
+ * (check_finite at optim.cpp:283-285 / :304-306), else 0. */
 int oracle_step_f64(int kind, const or_scalars* s, double* x, const double* g, double* m, double* v, size_t n);
 int oracle_undo_f64(int kind, const or_scalars* s, double* x, const double* g, double* m, double* v, size_t n);
 int oracle_step_f32(int kind, const or_scalars* s, float* x, const float* g, float* m, float* v, size_t n);
 int oracle_undo_f32(int kind, const or_scalars* s, float* x, const float* g, float* m, float* v, size_t n);
 
-/* AMSGrad step (optim.cpp:322-334) with its running max. */
+/* AMSGrad step (optim.cpp:244-256) with its running max. */
 int oracle_step_amsgrad_f64(const or_scalars* s, double* x, const double* g, double* m, double* v, double* vmax, size_t n);
 int oracle_step_amsgrad_f32(const or_scalars* s, float* x, const float* g, float* m, float* v, float* vmax, size_t n);
 
-/* LAMB (optim.cpp:273-320): step returns the trust ratio through *trust. */
+/* LAMB (optim.cpp:195-242): step returns the trust ratio through *trust. */
 int oracle_step_lamb_f64(const or_scalars* s, double* x, const double* g, double* m, double* v, size_t n, double* trust);
 int oracle_undo_lamb_f64(const or_scalars* s, double trust, double* x, const double* g, double* m, double* v, size_t n);
 
@@ -66,12 +66,5 @@ uint64_t oracle_mix64(uint64_t x);
 uint64_t oracle_derive_seed(uint64_t base, const uint64_t* parts, int n);
 void oracle_seeded_fill_f64(uint64_t seed, size_t n, double* out);
 void oracle_seeded_fill_f32(uint64_t seed, size_t n, float* out);
-
-/* Exhaustive check of "q = RN(a*r); e = fma(-q,b,a); q' = fma(e,r,q)" against
- * IEEE a/b for every fp32 mantissa of a in [1,2) (and hence, by exact binade
- * scaling, for every a in the kernel's fast-path range).  Returns the number
- * of mismatches.  Used to pin the constant-divisor fast path of the kernels. */
-uint64_t oracle_check_const_div_f32(float b, float lo_mant, float hi_mant);
-uint64_t oracle_check_const_div_f64_sampled(double b, uint64_t samples, uint64_t seed);
 
 #endif

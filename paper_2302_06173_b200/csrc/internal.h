@@ -3,7 +3,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "rewind_b200.h"
 
@@ -24,7 +26,7 @@ struct WorkItem {
 constexpr uint32_t kWorkCopyOnly = 1u;
 
 // t-dependent scalars of one call, derived in double on the host exactly as
-// optim.cpp does (lr_at :128-135, bias_correction :172-175, denom :184/:255).
+// optim.cpp does (lr_at :50-57, bias_correction :94-97, denom :106/:177).
 struct ScalarSet {
   double eta, c1, c2, denom;
 };
@@ -61,16 +63,29 @@ struct LaunchArgs {
   void* pv = nullptr;
 };
 
-// Kernel attributes (max dynamic smem) are per device: true the first time a
-// call site runs on the current device (mask bit per device index).
-inline bool first_on_device(unsigned long long& mask) {
-  int d = 0;
-  cudaGetDevice(&d);
-  const unsigned long long b = 1ull << (d & 63);
-  if (mask & b) return false;
-  mask |= b;
-  return true;
-}
+// One-time per-device setup of a call site (kernel attributes such as the
+// max dynamic smem, occupancy queries): `setup(device)` runs under a lock, and
+// the device's bit is published only after it succeeded, so a failed setup is
+// retried by the next call and no concurrent caller sees half-written values.
+class DeviceOnce {
+ public:
+  template <class F>
+  int run(F&& setup) {
+    int d = 0;
+    cudaGetDevice(&d);
+    const unsigned long long b = 1ull << (d & 63);
+    if (mask_.load(std::memory_order_acquire) & b) return 0;
+    std::lock_guard<std::mutex> lk(mu_);
+    if (mask_.load(std::memory_order_relaxed) & b) return 0;
+    const int e = setup(d);
+    if (e == 0) mask_.fetch_or(b, std::memory_order_release);
+    return e;
+  }
+
+ private:
+  std::mutex mu_;
+  std::atomic<unsigned long long> mask_{0};
+};
 
 // The CUDA runtime is shared with the caller (PyTorch), whose current device
 // may differ from the memory an entry point works on (PyTorch sets devices
@@ -121,7 +136,8 @@ int launch_clear_updated(rw_group* groups, const uint32_t* ids, uint32_t n, void
 // partial: 2 doubles per chunk.
 int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, const WorkItem* work,
                       uint32_t n_work, uint32_t total_chunks, uint32_t chunk_elems, ScalarSet* sets,
-                      const Uniform& u, double* partial, double* trust_table, uint32_t depth, void* stream);
+                      const Uniform& u, double* partial, double* trust_table, uint32_t depth, bool sequential,
+                      void* stream);
 
 // log_kernels.cu: CRC32 (wire.cpp:31-38) of a device buffer into *out_dev;
 // scratch = crc32_scratch_words(n) device uint32 words

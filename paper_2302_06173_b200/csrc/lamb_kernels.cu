@@ -1,4 +1,4 @@
-// LAMB step, first pass and trust ratio (optim.cpp:273-295).
+// LAMB step, first pass and trust ratio (optim.cpp:195-217).
 //
 // Pass 1 (all groups, one launch): advance m, v exactly as step_lamb does,
 // compute the update r + lambda x and accumulate ||x||^2 and ||update||^2 in
@@ -8,7 +8,7 @@
 // but it is not the reference's left-to-right sequential sum: the trust ratio
 // agrees to ~1e-15 relative (tolerance-matched; everything elementwise is
 // bit-exact).  The trust kernel (one CTA per group) stores the ratio (the LAMB
-// "saved scalar", optim.cpp:294) and writes scaled = eta * trust into the
+// "saved scalar", optim.cpp:216) and writes scaled = eta * trust into the
 // group's ScalarSet for the elementwise pass 2 (x update), which runs through
 // the fused TMA kernel.
 #include <cuda_runtime.h>
@@ -73,7 +73,7 @@ __device__ __forceinline__ void lamb_elem(const T* __restrict__ x, T* __restrict
                                           T* __restrict__ m, T* __restrict__ v, uint64_t k, const T c1, const T c2,
                                           const Uniform& u, double& sx, double& su) {
   const T gd = grad ? grad[k] : g[k];
-  if (grad) g[k] = gd;  // block.g = grad (optim.cpp:349)
+  if (grad) g[k] = gd;  // block.g = grad (optim.cpp:271)
   T mk = m[k], vk = v[k];
   lamb_math<T>(x[k], gd, mk, vk, c1, c2, u, sx, su);
   m[k] = mk;
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kLT) lamb_pass1_kernel(const T* __restrict__ x
       for (int e = 0; e < EV; ++e) lamb_math<T>(xp[e], gp[e], mp[e], vp[e], c1, c2, u, sx, su);
       *reinterpret_cast<VT*>(m + k) = mv;
       *reinterpret_cast<VT*>(v + k) = vv;
-      if (grad) *reinterpret_cast<VT*>(g + k) = gv;  // block.g = grad (optim.cpp:349)
+      if (grad) *reinterpret_cast<VT*>(g + k) = gv;  // block.g = grad (optim.cpp:271)
     }
     for (uint64_t k = b16 + lane; k < end; k += 32) lamb_elem<T>(x, g, grad, m, v, k, c1, c2, u, sx, su);
 #pragma unroll
@@ -140,8 +140,8 @@ __global__ void __launch_bounds__(kLT) lamb_pass1_kernel(const T* __restrict__ x
 }
 
 // One CTA per group: fixed-order reduction of its chunk partials -> trust
-// ratio (optim.cpp:288-290), saved (:294) and folded into the group's
-// ScalarSet as scaled = eta * trust for the x pass (:292).
+// ratio (optim.cpp:210-212), saved (:216) and folded into the group's
+// ScalarSet as scaled = eta * trust for the x pass (:214).
 __global__ void __launch_bounds__(kLT) lamb_trust_kernel(const WorkItem* __restrict__ work,
                                                          const double2* __restrict__ partial, double wd,
                                                          double* __restrict__ trust_table, uint32_t depth,
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kLT) lamb_trust_kernel(const WorkItem* __restr
   }
   if (threadIdx.x == 0) {
     const double xn = __dsqrt_rn(shx[0]), un = __dsqrt_rn(shu[0]);
-    const double trust = (xn > 0.0 && un > 0.0) ? __ddiv_rn(xn, un) : 1.0;  // optim.cpp:290
+    const double trust = (xn > 0.0 && un > 0.0) ? __ddiv_rn(xn, un) : 1.0;  // optim.cpp:212
     trust_table[uint64_t(w.gid) * depth + w.pad] = trust;
     ScalarSet* set = sets + w.sidx;
     set->eta = __dmul_rn(set->eta, trust);  // (eta * trust) * update
@@ -174,11 +174,43 @@ __global__ void __launch_bounds__(kLT) lamb_trust_kernel(const WorkItem* __restr
   }
 }
 
+// Reference-order norms (rw_state_set_flags(RW_STATE_LAMB_SEQUENTIAL_NORMS),
+// used by the host-block drop-in): one thread per group re-forms each
+// element's update from the m, v pass 1 just wrote (the same expression, so
+// the same bits) and accumulates ||x||^2 and ||update||^2 left to right in
+// fp64 exactly as step_lamb's loop does (optim.cpp:199-208).  The sums land in
+// the group's first chunk partial, zeros in the others, so the trust kernel's
+// tree adds only exact zeros and the ratio equals the reference's bit for bit.
+// O(n) on one thread: a parity path for host-resident blocks, not the batch path.
+template <typename T>
+__global__ void lamb_seq_norms_kernel(const T* __restrict__ x, const T* __restrict__ m, const T* __restrict__ v,
+                                      const WorkItem* __restrict__ work, const ScalarSet* __restrict__ sets,
+                                      Uniform u, double2* __restrict__ partial) {
+  using A = LA<T>;
+  const WorkItem w = work[blockIdx.x];
+  if (threadIdx.x != 0) return;
+  const ScalarSet ss = sets[w.sidx];
+  const T c1 = T(ss.c1), c2 = T(ss.c2);
+  double sx = 0.0, su = 0.0;
+  for (uint64_t k = w.off; k < w.off + w.len; ++k) {
+    const T xk = x[k];
+    const T mhat = A::div(m[k], c1);
+    const T vhat = A::div(v[k], c2);
+    const T upd = A::add(A::div(mhat, A::add(A::sqrt(vhat), T(u.eps))), A::mul(T(u.wd), xk));
+    const double xd = double(xk), ud = double(upd);
+    sx = __dadd_rn(sx, __dmul_rn(xd, xd));
+    su = __dadd_rn(su, __dmul_rn(ud, ud));
+  }
+  partial[w.chunk_begin] = make_double2(sx, su);
+  for (uint32_t i = 1; i < w.nchunks; ++i) partial[w.chunk_begin + i] = make_double2(0.0, 0.0);
+}
+
 }  // namespace
 
 int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, void* v, const WorkItem* work,
                       uint32_t n_work, uint32_t total_chunks, uint32_t chunk_elems, ScalarSet* sets,
-                      const Uniform& u, double* partial, double* trust_table, uint32_t depth, void* stream) {
+                      const Uniform& u, double* partial, double* trust_table, uint32_t depth, bool sequential,
+                      void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   if (n_work == 0 || total_chunks == 0) return 0;
   int dev = 0, sms = 148;
@@ -195,6 +227,14 @@ int launch_lamb_pass1(int dtype, void* x, void* g, const void* grad, void* m, vo
     lamb_pass1_kernel<float><<<grid, kLT, 0, st>>>(
         static_cast<const float*>(x), static_cast<float*>(g), static_cast<const float*>(grad),
         static_cast<float*>(m), static_cast<float*>(v), work, n_work, total_chunks, chunk_elems, sets, u, p2);
+  if (sequential) {
+    if (dtype == RW_F64)
+      lamb_seq_norms_kernel<double><<<n_work, 32, 0, st>>>(static_cast<const double*>(x), static_cast<const double*>(m),
+                                                           static_cast<const double*>(v), work, sets, u, p2);
+    else
+      lamb_seq_norms_kernel<float><<<n_work, 32, 0, st>>>(static_cast<const float*>(x), static_cast<const float*>(m),
+                                                          static_cast<const float*>(v), work, sets, u, p2);
+  }
   lamb_trust_kernel<<<n_work, kLT, 0, st>>>(work, p2, u.wd, trust_table, depth, sets);
   return static_cast<int>(cudaGetLastError());
 }

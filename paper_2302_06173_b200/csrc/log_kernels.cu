@@ -217,12 +217,12 @@ int launch_crc32(const void* data, uint64_t n, uint32_t* out_dev, uint32_t* scra
   auto st = static_cast<cudaStream_t>(stream);
   const CrcOps& ops = crc_ops();
   const uint64_t nchunks = n / kChunk;
-  static unsigned long long dev_mask = 0;
-  if (first_on_device(dev_mask)) {
-    const cudaError_t e = cudaFuncSetAttribute(crc_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(kChunkSmem));
-    if (e != cudaSuccess) return static_cast<int>(e);
-  }
+  static DeviceOnce once;
+  const int se = once.run([](int) {
+    return static_cast<int>(cudaFuncSetAttribute(crc_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(kChunkSmem)));
+  });
+  if (se) return se;
   if (nchunks) {
     crc_chunks_kernel<<<static_cast<unsigned>(nchunks), kCrcThreads, kChunkSmem, st>>>(
         static_cast<const uint8_t*>(data), n, ops.tree, scratch);

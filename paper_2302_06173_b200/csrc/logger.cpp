@@ -302,17 +302,17 @@ int rw_crc32_device(const void* data, uint64_t n, uint32_t* out_dev, void* strea
   // the scratch comes from the device's default stream-ordered pool; keep a
   // few MB of it cached (release threshold) so a call does not map and unmap
   // memory each time (the default threshold of 0 returns it at every sync)
-  static unsigned long long pool_mask = 0;
-  if (rwb::first_on_device(pool_mask)) {
-    int dev = 0;
+  static rwb::DeviceOnce pool_once;
+  pool_once.run([](int dev) {
     cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t keep = 64ull << 20;
       uint64_t cur = 0;
       if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < keep)
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-  }
+    return 0;  // best effort: the threshold only saves remapping
+  });
   uint32_t* scratch = nullptr;
   LCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), rwb::crc32_scratch_words(n) * 4,
                         static_cast<cudaStream_t>(stream)));
@@ -436,6 +436,8 @@ int rw_logger_flush(rw_logger* L, uint64_t* committed) {
   if (L->err) return lfail(L->err, L->errmsg);
   return RW_OK;
 }
+
+void* rw_logger_stream(rw_logger* L) { return L ? static_cast<void*>(L->copy_stream) : nullptr; }
 
 int rw_logger_destroy(rw_logger* L) {
   if (!L) return RW_OK;

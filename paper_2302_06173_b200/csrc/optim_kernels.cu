@@ -6,11 +6,11 @@
 // operation an explicit round-to-nearest intrinsic so no FMA contraction can
 // occur regardless of -fmad (the library is also built with -fmad=false).
 // The same pass:
-//   * caches the incoming gradient into g (optim.cpp:349, `block.g = grad`),
-//   * evaluates check_finite on x, m, v (optim.cpp:361-363 / :382-384) as a
+//   * caches the incoming gradient into g (optim.cpp:271, `block.g = grad`),
+//   * evaluates check_finite on x, m, v (optim.cpp:283-285 / :304-306) as a
 //     per-group non-finite flag (no extra HBM pass),
 //   * rewrites the group's update-progress marker (t, updated;
-//     optim.cpp:359-360 / :380-381) once the group's last tile is stored.
+//     optim.cpp:281-282 / :302-303) once the group's last tile is stored.
 //
 // Data movement (the kernel is HBM-bound: 28 B/param for Adam fp32):
 //   x, g, m, v are separate flat arrays (SoA).  The state is cut into tiles
@@ -81,20 +81,20 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
   using A = Arith<T>;
   if constexpr (KIND == RW_SGD) {
     if constexpr (!UNDO) {
-      // optim.cpp:179  x -= eta * (g + wd * x)
+      // optim.cpp:101  x -= eta * (g + wd * x)
       x = A::sub(x, A::mul(s.eta, A::add(g, A::mul(s.wd, x))));
     } else {
-      // optim.cpp:187  x = (x + eta * g) / denom
+      // optim.cpp:109  x = (x + eta * g) / denom
       x = A::div(A::add(x, A::mul(s.eta, g)), s.denom);
     }
   } else if constexpr (KIND == RW_SGDM) {
     if constexpr (!UNDO) {
-      // optim.cpp:193-195
+      // optim.cpp:115-117
       T gd = A::add(g, A::mul(s.wd, x));
       m = A::add(A::mul(s.mu, m), A::mul(s.omd, gd));
       x = A::sub(x, A::mul(s.eta, m));
     } else {
-      // optim.cpp:202-205
+      // optim.cpp:124-127
       T xt = A::add(x, A::mul(s.eta, m));
       T gd = A::add(g, A::mul(s.wd, xt));
       m = A::div(A::sub(m, A::mul(s.omd, gd)), s.mu);
@@ -102,7 +102,7 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
     }
   } else if constexpr (KIND == RW_ADAM || KIND == RW_AMSGRAD) {
     if constexpr (!UNDO) {
-      // optim.cpp:212-217 (Adam) / :326-332 (AMSGrad)
+      // optim.cpp:134-139 (Adam) / :248-254 (AMSGrad)
       T gd = A::add(g, A::mul(s.wd, x));
       m = A::add(A::mul(s.b1, m), A::mul(s.omb1, gd));
       v = A::add(A::mul(s.b2, v), A::mul(A::mul(s.omb2, gd), gd));
@@ -115,7 +115,7 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
       T vhat = A::div(den_src, s.c2);
       x = A::sub(x, A::div(A::mul(s.eta, mhat), A::add(A::sqrt(vhat), s.eps)));
     } else {
-      // optim.cpp:227-233 (Adam only; AMSGrad undo is refused on the host)
+      // optim.cpp:149-155 (Adam only; AMSGrad undo is refused on the host)
       T mhat = A::div(m, s.c1);
       T vhat = A::div(v, s.c2);
       T xt = A::add(x, A::div(A::mul(s.eta, mhat), A::add(A::sqrt(vhat), s.eps)));
@@ -126,7 +126,7 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
     }
   } else if constexpr (KIND == RW_ADAMW) {
     if constexpr (!UNDO) {
-      // optim.cpp:241-247
+      // optim.cpp:163-169
       T gd = g;
       m = A::add(A::mul(s.b1, m), A::mul(s.omb1, gd));
       v = A::add(A::mul(s.b2, v), A::mul(A::mul(s.omb2, gd), gd));
@@ -135,7 +135,7 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
       x = A::sub(x, A::mul(s.eta, A::add(A::div(mhat, A::add(A::sqrt(vhat), s.eps)),
                                          A::mul(s.wd, x))));
     } else {
-      // optim.cpp:259-265
+      // optim.cpp:181-187
       T mhat = A::div(m, s.c1);
       T vhat = A::div(v, s.c2);
       T xt = A::div(A::add(x, A::div(A::mul(s.eta, mhat), A::add(A::sqrt(vhat), s.eps))),
@@ -148,14 +148,14 @@ __device__ __forceinline__ void elem(const Sc<T>& s, T& x, T g, T& m, T& v, T& v
   } else if constexpr (KIND == RW_LAMB) {
     // s.eta carries scaled = eta * trust (the saved ratio) for LAMB.
     if constexpr (!UNDO) {
-      // second pass of step_lamb, optim.cpp:282-293: m, v already advanced
+      // second pass of step_lamb, optim.cpp:204-215: m, v already advanced
       // by lamb_pass1_kernel; x -= (eta * trust) * update
       T mhat = A::div(m, s.c1);
       T vhat = A::div(v, s.c2);
       T u = A::add(A::div(mhat, A::add(A::sqrt(vhat), s.eps)), A::mul(s.wd, x));
       x = A::sub(x, A::mul(s.eta, u));
     } else {
-      // optim.cpp:309-318 with scaled = eta * trust, denom = 1 - scaled * wd
+      // optim.cpp:231-240 with scaled = eta * trust, denom = 1 - scaled * wd
       T mhat = A::div(m, s.c1);
       T vhat = A::div(v, s.c2);
       T r = A::div(mhat, A::add(A::sqrt(vhat), s.eps));
@@ -551,17 +551,19 @@ int launch_t(const LaunchArgs& a, cudaStream_t st) {
   constexpr size_t smem = dyn_smem_bytes<T, KIND, PUSH>();
   static int blocks_per_sm = -1;  // per instantiation (same on every B200)
   static int num_sms = -1;
-  static unsigned long long dev_mask = 0;
-  if (first_on_device(dev_mask)) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+  static DeviceOnce once;
+  const int se = once.run([&](int dev) {
+    int sms = 0, bps = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, kThreads, smem);
     if (e != cudaSuccess) return static_cast<int>(e);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kThreads, smem);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+    num_sms = sms;
+    blocks_per_sm = bps < 1 ? 1 : bps;
+    return 0;
+  });
+  if (se) return se;
   uint32_t grid = static_cast<uint32_t>(num_sms * blocks_per_sm);
   if (grid > a.total_chunks) grid = a.total_chunks;
   if (grid == 0) return 0;

@@ -39,7 +39,7 @@ int rw_stage_forward(const rw_stage_desc* st, int64_t rows, void* const* acts, v
   int s = check_desc(st, rows);
   if (s) return s;
   if (!acts) return rfail(RW_INVALID_ARGUMENT, "null activations");
-  for (int l = 0; l < st->num_layers; ++l) {  // model.cpp:156-159, layer order
+  for (int l = 0; l < st->num_layers; ++l) {  // model.cpp:84-87, layer order
     if (!acts[l] || !acts[l + 1]) return rfail(RW_MISSING_ACTIVATION, "MissingActivation: null activation buffer");
     int e = rwb::replay_forward_layer(acts[l], rows, st->dims[l], st->dims[l + 1], st->w[l], st->b[l], acts[l + 1],
                                       stream);
@@ -79,7 +79,7 @@ int rw_stage_backward_ex2(const rw_stage_desc* st, int64_t rows, void* const* ac
   for (int l = 0; l <= st->num_layers; ++l)
     if (!acts[l]) return rfail(RW_MISSING_ACTIVATION, "MissingActivation: no cached forward for micro-batch");
   const int L = st->num_layers;
-  // dz of the last layer: dL/dy * (1 - y^2)  (model.cpp:185-192) -- or
+  // dz of the last layer: dL/dy * (1 - y^2)  (model.cpp:113-120) -- or
   // already fused into the next stage's first-layer dgrad (grad_in_is_dz)
   void* cur = dz0;
   void* nxt = dz1;
@@ -94,7 +94,7 @@ int rw_stage_backward_ex2(const rw_stage_desc* st, int64_t rows, void* const* ac
   // (per 32-row block, into scratch) when the scratch holds ceil(rows/32) rows
   const int64_t nsplit = (rows + 31) / 32;
   bool cur_fused = false;
-  for (int li = L - 1; li >= 0; --li) {  // reverse layer order (model.cpp:179)
+  for (int li = L - 1; li >= 0; --li) {  // reverse layer order (model.cpp:107)
     const int64_t in = st->dims[li], out = st->dims[li + 1];
     // dW = x^T dz (:193-203), accumulated over micro-batches in order
     e = rwb::replay_wgrad_layer(acts[li], cur, rows, in, out, dw[li], accumulate, stream);

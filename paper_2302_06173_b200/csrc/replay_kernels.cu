@@ -26,7 +26,7 @@ constexpr int kBN = 256;
 constexpr int kPairDefault = 0;
 
 __device__ __forceinline__ bf16 dtanh1(bf16 g, bf16 y) {
-  // dz = dL/dy * (1 - y^2)   (model.cpp:185-192)
+  // dz = dL/dy * (1 - y^2)   (model.cpp:113-120)
   const float yv = __bfloat162float(y);
   return __float2bfloat16_rn(__fmul_rn(__bfloat162float(g), __fsub_rn(1.f, __fmul_rn(yv, yv))));
 }

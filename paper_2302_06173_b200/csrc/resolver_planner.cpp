@@ -36,7 +36,7 @@ extern "C" {
 //
 // Spec gap: SPEC:487 undoes blocks whose flag is set OR
 // whose t is beyond the target, but optimizer_undo refuses !updated blocks
-// (optim.cpp:367).  We decide on t alone and re-arm the flag before undoing
+// (optim.cpp:289).  We decide on t alone and re-arm the flag before undoing
 // (rw_apply in the Python/C++ drivers), allowing at most one step of undo.
 int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad_ready,
                          const rw_hyper* h, uint64_t t_floor, rw_resolve_summary* out) {
@@ -48,7 +48,9 @@ int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad
     if (groups[i].t < s.t_min) s.t_min = groups[i].t;
     if (groups[i].t > s.t_max) s.t_max = groups[i].t;
   }
-  if (n == 0) s.t_min = 0;
+  // n == 0 (a replacement with no state yet): t_min stays UINT64_MAX and
+  // t_max 0, the identities of the MIN / MAX all-reduces, so a joining rank
+  // never drags the consensus down.
   // phase 1: t_floor == UINT64_MAX -> relative to the local minimum;
   // phase 2: relative to the all-reduced (global MIN) t_floor.
   const uint64_t lo = t_floor == UINT64_MAX ? s.t_min : t_floor;
@@ -59,8 +61,8 @@ int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad
       if (!grad_ready || !grad_ready[i]) s.redo_blocked += 1;
     }
   }
-  // undo_<kind> hyper guards (optim.cpp:184, :200, :222, :252-256) and the
-  // AMSGrad refusal (:368-370).  LAMB undoes with its saved trust ratio
+  // undo_<kind> hyper guards (optim.cpp:106, :122, :144, :174-178) and the
+  // AMSGrad refusal (:290-292).  LAMB undoes with its saved trust ratio
   // (:297-320); a group whose ratio is missing fails at apply time.
   bool blocked = rw_invertibility_check(h->kind) == RW_NOT_INVERTIBLE_KIND;
   if (h->kind == RW_SGDM && h->momentum == 0.0) blocked = true;

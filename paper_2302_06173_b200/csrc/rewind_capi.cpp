@@ -1,10 +1,10 @@
 // Host side of the C ABI (include/rewind_b200.h): guards, scalar derivation,
 // marker bookkeeping and launch of the fused kernels.  Mirrors the control
-// flow of optimizer_step / optimizer_undo (optim.cpp:338-385) group by group.
+// flow of optimizer_step / optimizer_undo (optim.cpp:260-307) group by group.
 //
 // Build note: compiled with -ffp-contract=off so the double scalars below are
-// the same IEEE expressions the reference evaluates (optim.cpp:172-175, :184,
-// :255) — glibc pow for the bias corrections, exactly as the reference.
+// the same IEEE expressions the reference evaluates (optim.cpp:94-97, :106,
+// :177) — glibc pow for the bias corrections, exactly as the reference.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -61,7 +61,7 @@ const char* kind_name(int k) {
   return "?";
 }
 
-// OptimizerHyper::lr_at, optim.cpp:128-135
+// OptimizerHyper::lr_at, optim.cpp:50-57
 int lr_at(const rw_hyper* h, uint64_t t, double* out) {
   double v = h->lr;
   for (uint32_t i = 0; i < h->lr_table_len; ++i)
@@ -111,7 +111,7 @@ struct rw_state {
   rw_group* d_groups = nullptr;
   Slot slots[kSlots];
   int next_slot = 0;
-  // LAMB saved scalars (ParamBlock::saved_scalars, optim.cpp:294): a per-group
+  // LAMB saved scalars (ParamBlock::saved_scalars, optim.cpp:216): a per-group
   // ring of the last kTrustDepth trust ratios, written by lamb_trust_kernel;
   // head/count are host-side so the stack top is known without a sync.
   double* d_trust = nullptr;       // [G * kTrustDepth]
@@ -119,6 +119,7 @@ struct rw_state {
   uint64_t partial_cap = 0;
   std::vector<uint64_t> trust_head;
   std::vector<uint32_t> trust_count;
+  uint32_t flags = 0;  // RW_STATE_* (rw_state_set_flags)
   // host-resident undo pipeline (rw_optimizer_undo_host)
   cudaStream_t h2d = nullptr;
   cudaStream_t d2h = nullptr;
@@ -243,7 +244,8 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
       }
       int e = rwb::launch_lamb_pass1(s->dtype, s->x, s->g, grad == s->g ? nullptr : grad, s->m, s->v, sl.d_work,
                                      n_items, static_cast<uint32_t>(chunk), ce, sl.d_sets, uniform_of(h),
-                                     s->d_partial, s->d_trust, kTrustDepth, stream);
+                                     s->d_partial, s->d_trust, kTrustDepth,
+                                     (s->flags & RW_STATE_LAMB_SEQUENTIAL_NORMS) != 0, stream);
       if (e) return cuda_fail(static_cast<cudaError_t>(e), "lamb pass 1");
       grad = nullptr;  // pass 1 cached it in g
     }
@@ -280,7 +282,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     rw_group& gr = s->mirror[ids[i]];
     gr.t = undo ? gr.t - 1 : gr.t + 1;
     gr.updated = undo ? 0u : 1u;
-    if (lamb) {  // push / pop the saved trust ratio (optim.cpp:294 / :319)
+    if (lamb) {  // push / pop the saved trust ratio (optim.cpp:216 / :241)
       const uint32_t g = ids[i];
       if (undo) {
         s->trust_head[g] -= 1;
@@ -298,7 +300,7 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
 
 size_t elem_size(int dtype) { return dtype == RW_F64 ? 8 : 4; }
 
-// undo_lamb guards (optim.cpp:297-308) for the groups ids[0..n): the saved
+// undo_lamb guards (optim.cpp:219-230) for the groups ids[0..n): the saved
 // trust ratio must exist; etas[i] (lr_at(t)) becomes scaled = eta * trust and
 // denom = 1 - scaled * wd must not vanish.  One D2H read of the trust table.
 int lamb_undo_scalars(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, std::vector<double>& etas,
@@ -357,7 +359,7 @@ int rw_invertibility_check(int32_t kind) {
   }
 }
 
-// OptimizerHyper::validate, optim.cpp:137-149 (same checks, same order)
+// OptimizerHyper::validate, optim.cpp:59-71 (same checks, same order)
 int rw_hyper_validate(const rw_hyper* h) {
   if (!h) return fail(RW_INVALID_ARGUMENT, "null hyper");
   if (!(h->lr > 0.0)) return fail(RW_INVALID_CONFIG, "InvalidConfig: optimizer.lr must be > 0");
@@ -446,6 +448,13 @@ void rw_state_destroy(rw_state* s) {
   if (s->d2h) cudaStreamSynchronize(s->d2h), cudaStreamDestroy(s->d2h);
   for (cudaEvent_t e : s->evs) cudaEventDestroy(e);
   delete s;
+}
+
+int rw_state_set_flags(rw_state* s, uint32_t flags) {
+  if (!s) return fail(RW_INVALID_ARGUMENT, "null state");
+  if (flags & ~uint32_t(RW_STATE_LAMB_SEQUENTIAL_NORMS)) return fail(RW_INVALID_ARGUMENT, "unknown state flag");
+  s->flags = flags;
+  return RW_OK;
 }
 
 uint32_t rw_state_num_groups(const rw_state* s) { return s ? static_cast<uint32_t>(s->mirror.size()) : 0; }
@@ -564,7 +573,7 @@ int rw_clear_updated(rw_state* s, const uint32_t* ids, uint32_t n, void* stream)
   return RW_OK;
 }
 
-// optimizer_step, optim.cpp:338-364
+// optimizer_step, optim.cpp:260-286
 int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n,
                       const void* grad, uint32_t stop_after, void* stream) {
   rwb::DeviceScope dev_scope(s ? s->device : -1);
@@ -606,7 +615,7 @@ int rw_optimizer_step(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint3
 }  // extern "C"
 
 namespace {
-// The guards of optimizer_undo (optim.cpp:366-385) and of undo_<kind>, for
+// The guards of optimizer_undo (optim.cpp:288-307) and of undo_<kind>, for
 // every group, before anything is launched; fills the per-group eta (LAMB:
 // eta * saved trust ratio).
 int undo_prepare(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, std::vector<double>& etas,
@@ -625,7 +634,7 @@ int undo_prepare(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n
     if (st) return st;
     const double eta = etas[i];
     switch (h->kind) {
-      case RW_SGD:  // optim.cpp:184-185
+      case RW_SGD:  // optim.cpp:106-107
         if (1.0 - eta * h->weight_decay == 0.0)
           return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1 for sgd");
         break;
@@ -642,7 +651,7 @@ int undo_prepare(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n
         if (1.0 - eta * h->weight_decay == 0.0)
           return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: lr*weight_decay == 1 for adamw");
         break;
-      case RW_LAMB:  // optim.cpp:297-303; the trust read + denom check follow the loop
+      case RW_LAMB:  // optim.cpp:219-225; the trust read + denom check follow the loop
         if (h->beta1 == 0.0 || h->beta2 == 0.0)
           return fail(RW_NON_INVERTIBLE_HYPER, "NonInvertibleHyper: beta1*beta2 == 0 for lamb");
         if (s->trust_count[ids[i]] == 0)
@@ -661,7 +670,7 @@ int undo_prepare(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n
 
 extern "C" {
 
-// optimizer_undo, optim.cpp:366-385 and the per-kind guards of undo_<kind>
+// optimizer_undo, optim.cpp:288-307 and the per-kind guards of undo_<kind>
 int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n, void* stream) {
   rwb::DeviceScope dev_scope(s ? s->device : -1);
   std::vector<double> etas;
@@ -897,7 +906,9 @@ int stage_prepare(int dtype, uint64_t n) {
   const size_t bytes = n * elem_size(dtype);
   for (auto& p : S.d) RW_CUDA(cudaMalloc(&p, bytes));
   rw_group gr{0, n, 0, 0, 0};
-  return rw_state_create(&S.st, dtype, S.d[0], S.d[1], S.d[2], S.d[3], S.d[4], n, &gr, 1, dev);
+  const int st = rw_state_create(&S.st, dtype, S.d[0], S.d[1], S.d[2], S.d[3], S.d[4], n, &gr, 1, dev);
+  // the host-block drop-in reproduces step_lamb's left-to-right norms (bit-exact trust ratio)
+  return st ? st : rw_state_set_flags(S.st, RW_STATE_LAMB_SEQUENTIAL_NORMS);
 }
 
 int block_guards_step(const rw_hyper* h, uint64_t t, uint32_t updated, double* eta) {
@@ -911,7 +922,7 @@ int block_guards_step(const rw_hyper* h, uint64_t t, uint32_t updated, double* e
 
 extern "C" {
 
-// optimizer_step on a host ParamBlock (optim.cpp:338-364)
+// optimizer_step on a host ParamBlock (optim.cpp:260-286)
 int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* vmax, uint64_t n,
                        uint64_t* t, uint32_t* updated, const void* grad, const rw_hyper* h) {
   if (!x || !g || !t || !updated || !h || !grad) return fail(RW_INVALID_ARGUMENT, "null argument");
@@ -945,12 +956,12 @@ int rw_host_block_step(int32_t dtype, void* x, void* g, void* m, void* v, void* 
   void* outs[5] = {x, g, m, v, vmax};
   for (int i = 0; i < 5; ++i)
     if (use[i]) RW_CUDA(cudaMemcpyAsync(outs[i], S.d[i], bytes, cudaMemcpyDeviceToHost, S.stream));
-  *t += 1;  // optim.cpp:359-360
+  *t += 1;  // optim.cpp:281-282
   *updated = 1;
   return rw_state_check(S.st, S.stream);  // :361-363, after mutation
 }
 
-// optimizer_undo on a host ParamBlock (optim.cpp:366-385)
+// optimizer_undo on a host ParamBlock (optim.cpp:288-307)
 int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64_t n, uint64_t* t,
                        uint32_t* updated, const rw_hyper* h) {
   if (!x || !g || !t || !updated || !h) return fail(RW_INVALID_ARGUMENT, "null argument");
@@ -982,7 +993,7 @@ int rw_host_block_undo(int32_t dtype, void* x, void* g, void* m, void* v, uint64
   const bool out[4] = {true, false, um, uv};
   for (int i = 0; i < 4; ++i)
     if (out[i]) RW_CUDA(cudaMemcpyAsync(hs[i], S.d[i], bytes, cudaMemcpyDeviceToHost, S.stream));
-  *t -= 1;  // optim.cpp:380-381
+  *t -= 1;  // optim.cpp:302-303
   *updated = 0;
   return rw_state_check(S.st, S.stream);  // :382-384, after mutation
 }

@@ -100,15 +100,12 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
       return static_cast<int>(cudaErrorNotSupported);
   }
   auto kern = umma_gemm_kernel<BN, AMAJ, BMAJ, EPI>;
-  static unsigned long long dev_mask = 0;  // the attribute is per device
-  int cur_dev = 0;
-  cudaGetDevice(&cur_dev);
-  if (!(dev_mask & (1ull << (cur_dev & 63)))) {
-    cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(Cfg<BN>::kSmem));
-    if (ce != cudaSuccess) return static_cast<int>(ce);
-    dev_mask |= 1ull << (cur_dev & 63);
-  }
+  static DeviceOnce once;  // the attribute is per device
+  const int se = once.run([&](int) {
+    return static_cast<int>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(Cfg<BN>::kSmem)));
+  });
+  if (se) return se;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -140,15 +137,12 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
       return static_cast<int>(cudaErrorNotSupported);
   }
   auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI>;
-  static unsigned long long dev_mask = 0;  // the attribute is per device
-  int cur_dev = 0;
-  cudaGetDevice(&cur_dev);
-  if (!(dev_mask & (1ull << (cur_dev & 63)))) {
-    cudaError_t ce = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(Cfg2<BN>::kSmem));
-    if (ce != cudaSuccess) return static_cast<int>(ce);
-    dev_mask |= 1ull << (cur_dev & 63);
-  }
+  static DeviceOnce once;  // the attribute is per device
+  const int se = once.run([&](int) {
+    return static_cast<int>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 static_cast<int>(Cfg2<BN>::kSmem)));
+  });
+  if (se) return se;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -10,6 +10,7 @@ returning a ``replay.BoundaryLog`` keyed by (iteration, micro-batch).
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import glob
 import os
@@ -38,6 +39,7 @@ for _n, (_r, _a) in {
     "rw_logger_log": (C.c_int, [_vp, C.POINTER(rw_log_record), _vp, _vp]),
     "rw_logger_flush": (C.c_int, [_vp, C.POINTER(_u64)]),
     "rw_logger_destroy": (C.c_int, [_vp]),
+    "rw_logger_stream": (_vp, [_vp]),
     "rw_log_open": (C.c_int, [C.POINTER(_vp), C.c_char_p, C.POINTER(_u32)]),
     "rw_log_next": (C.c_int, [_vp, C.POINTER(rw_log_record), _vp, _u64, C.POINTER(C.c_int32)]),
     "rw_log_close": (None, [_vp]),
@@ -72,7 +74,11 @@ class Logger:
         dev = torch.cuda.current_device() if device is None else device
         check(LIB.rw_logger_create(C.byref(self._h), directory.encode(), machine, chunk_records, pinned_bytes,
                                    dev))
-        self._keep: list[torch.Tensor] = []
+        # payloads in flight: (event on the logger's copy stream after the
+        # record's D2H, tensor).  Trimmed on every log_send as the copies
+        # complete, so device memory is held only while the D2H still reads it.
+        self._copy_stream = torch.cuda.ExternalStream(LIB.rw_logger_stream(self._h), device=dev)
+        self._inflight: collections.deque = collections.deque()
 
     def log_send(self, t: torch.Tensor, sender: int, receiver: int, iteration: int, mb: int, direction: int,
                  stream=None) -> None:
@@ -88,19 +94,23 @@ class Logger:
             r.shape[i] = s
         r.payload_bytes = t.numel() * t.element_size()
         check(LIB.rw_logger_log(self._h, C.byref(r), _vp(t.data_ptr()), _stream(stream)))
-        self._keep.append(t)  # keep alive until flush (the D2H reads it asynchronously)
+        ev = torch.cuda.Event()
+        ev.record(self._copy_stream)  # after this record's CRC + D2H on the logger stream
+        self._inflight.append((ev, t))
+        while self._inflight and self._inflight[0][0].query():
+            self._inflight.popleft()
 
     def flush(self) -> int:
         n = _u64()
         check(LIB.rw_logger_flush(self._h, C.byref(n)))
-        self._keep.clear()
+        self._inflight.clear()  # flush waited for every copy
         return n.value
 
     def close(self) -> None:
         if self._h.value:
             st = LIB.rw_logger_destroy(self._h)
             self._h = _vp()
-            self._keep.clear()
+            self._inflight.clear()
             check(st)
 
     def __del__(self):

@@ -31,12 +31,12 @@ TRUST_DEPTH = 8  # RW_LAMB_TRUST_DEPTH (include/rewind_b200.h)
 
 
 def optimizer_from_name(name: str) -> int | None:
-    """optimizer_from_name, optim.cpp:103-111."""
+    """optimizer_from_name, optim.cpp:25-33."""
     return _KIND_NAMES.get(name)
 
 
 def invertibility_check(kind: int) -> int:
-    """invertibility_check, optim.hpp:32 / optim.cpp:113-126."""
+    """invertibility_check, optim.hpp:32 / optim.cpp:35-48."""
     return LIB.rw_invertibility_check(kind)
 
 
@@ -75,13 +75,13 @@ class OptimizerHyper:
         return h
 
     def lr_at(self, t: int) -> float:
-        """OptimizerHyper::lr_at, optim.cpp:128-135."""
+        """OptimizerHyper::lr_at, optim.cpp:50-57."""
         out = C.c_double()
         check(LIB.rw_lr_at(C.byref(self.to_c()), t, C.byref(out)))
         return out.value
 
     def validate(self) -> None:
-        """OptimizerHyper::validate, optim.cpp:137-149."""
+        """OptimizerHyper::validate, optim.cpp:59-71."""
         check(LIB.rw_hyper_validate(C.byref(self.to_c())))
 
 
@@ -236,7 +236,7 @@ class DeviceState:
         check(LIB.rw_state_write_groups(self._h, g, C.c_void_p(_stream_handle(stream))))
 
     def saved_scalars(self, i: int, stream=None) -> list[float]:
-        """LAMB trust-ratio stack of group i, bottom -> top (optim.cpp:294)."""
+        """LAMB trust-ratio stack of group i, bottom -> top (optim.cpp:216)."""
         buf = (C.c_double * TRUST_DEPTH)()
         cnt = C.c_uint32()
         check(LIB.rw_state_saved_scalars(self._h, i, buf, TRUST_DEPTH, C.byref(cnt),

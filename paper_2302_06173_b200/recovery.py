@@ -83,7 +83,7 @@ def resolve(markers: Sequence[tuple[int, int]], hyper, lens: Sequence[int] | Non
         ready = (C.c_uint8 * max(n, 1))(*[1 if r else 0 for r in grad_ready])
     loc = rw_resolve_summary()
     check(LIB.rw_resolve_summarize(g, n, ready, C.byref(h), U64_MAX, C.byref(loc)))
-    t_min = loc.t_min if n else U64_MAX >> 1
+    t_min = min(loc.t_min, U64_MAX >> 1)  # n == 0 -> UINT64_MAX (MIN identity), int64-safe
     lo = _allreduce_u64([t_min], dist.ReduceOp.MIN if dist.is_available() else None, group, device)[0]
     hi = _allreduce_u64([loc.t_max], dist.ReduceOp.MAX if dist.is_available() else None, group,
                         device)[0]

@@ -1,11 +1,11 @@
 """Logging-based replay on the B200.
 
 Reference semantics (model.cpp; recovery.cpp is absent):
-  * a Stage is `num_layers` affine+tanh layers (make_stage, model.cpp:104-126),
-    params in blocks() order W0, b0, W1, b1, ... (model.cpp:84-92);
+  * a Stage is `num_layers` affine+tanh layers (make_stage, model.cpp:32-54),
+    params in blocks() order W0, b0, W1, b1, ... (model.cpp:12-20);
   * an iteration runs every micro-batch forward + backward, accumulates the
     per-micro-batch gradients in ascending micro-batch order (accumulate_grads,
-    model.cpp:230-244) and then steps every block in reverse layer order
+    model.cpp:158-172) and then steps every block in reverse layer order
     (apply_layerwise_updates);
   * recover_replay: the replacement loads the checkpoint and
     re-executes its stages feeding the logged inbound activations / gradients
@@ -77,14 +77,14 @@ def _p(t: torch.Tensor | None) -> C.c_void_p:
 
 def synth_inputs(seed: int, iteration: int, stream: int, rows: int, dim: int,
                  dtype=torch.bfloat16, device=None) -> torch.Tensor:
-    """synth_inputs (model.cpp:262-265): seeded_fill of derive_seed(seed, {1, it, stream})."""
+    """synth_inputs (model.cpp:190-193): seeded_fill of derive_seed(seed, {1, it, stream})."""
     out = torch.empty(rows, dim, dtype=dtype, device=device or torch.cuda.current_device())
     _fill(out, derive_seed(seed, [1, iteration, stream]))
     return out
 
 
 def synth_targets(seed: int, iteration: int, stream: int, rows: int, dim: int, device=None) -> torch.Tensor:
-    """synth_targets (model.cpp:267-270), fp32."""
+    """synth_targets (model.cpp:195-198), fp32."""
     out = torch.empty(rows, dim, dtype=torch.float32, device=device or torch.cuda.current_device())
     _fill(out, derive_seed(seed, [2, iteration, stream]))
     return out
@@ -101,7 +101,7 @@ class Stage:
     def __init__(self, stage_id: int, input_dim: int, hidden_dim: int, output_dim: int, num_layers: int,
                  seed: int, kind: int, device=None, dims: Sequence[int] | None = None):
         """make_stage(stage_id, input_dim, hidden_dim, output_dim, num_layers, seed)
-        (model.cpp:104-126).  `dims` (num_layers + 1 widths) generalises the
+        (model.cpp:32-54).  `dims` (num_layers + 1 widths) generalises the
         uniform hidden width, e.g. MLP blocks 4096 -> 11008 -> 4096 -> ..."""
         if num_layers < 1:
             raise RwError(18, "InvalidConfig: stage needs >= 1 layer")
@@ -118,7 +118,7 @@ class Stage:
         self.state = DeviceState(sizes, dtype=torch.float32, kind=kind, device=device)
         dev = self.state.device
         self.device = dev
-        # make_stage (model.cpp:117-122): W_l from derive_seed(seed,{id,l,0}), b_l from {id,l,1}
+        # make_stage (model.cpp:45-50): W_l from derive_seed(seed,{id,l,0}), b_l from {id,l,1}
         for l in range(num_layers):
             seeded_fill_(self.state.view("x", 2 * l), derive_seed(seed, [stage_id, l, 0]))
             seeded_fill_(self.state.view("x", 2 * l + 1), derive_seed(seed, [stage_id, l, 1]))
@@ -219,7 +219,7 @@ class Stage:
 
 def mse_grad(pred: torch.Tensor, target: torch.Tensor, micro_batches: int,
              loss: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """mse_loss gradient (model.cpp:246-260) on the device: bf16 grad, fp64 loss."""
+    """mse_loss gradient (model.cpp:174-188) on the device: bf16 grad, fp64 loss."""
     grad = torch.empty_like(pred)
     scratch = torch.empty(256, dtype=torch.float64, device=pred.device)
     check(LIB.rw_mse_grad(_p(pred), _p(target), pred.numel(), micro_batches, _p(grad), _p(loss), _p(scratch),
@@ -450,7 +450,7 @@ def _shard_bounds(P: int, d: int) -> tuple[int, list[tuple[int, int]]]:
     return chunk, [(min(P, j * chunk), min(P, (j + 1) * chunk)) for j in range(d)]
 
 
-def ordered_merge_start(bufs: dict, P: int, m: int, group=None):
+def ordered_merge_start(bufs: dict, P: int, m: int, group=None, device=None):
     """Start the ordered merge of one stage's gradient over the d
     helpers: the flat gradient is sharded over the ranks; every owner sends
     shard j of each of its micro-batches to rank j in ONE grouped batch of
@@ -461,7 +461,8 @@ def ordered_merge_start(bufs: dict, P: int, m: int, group=None):
     glob = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)  # noqa: E731
     chunk, bnd = _shard_bounds(P, d)
     lo, hi = bnd[rank]
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = device if device is not None else (next(iter(bufs.values())).device if bufs else
+                                              torch.device("cuda", torch.cuda.current_device()))
     recv, ops = {}, []
     for mb in range(m):
         owner = mb % d
@@ -476,21 +477,29 @@ def ordered_merge_start(bufs: dict, P: int, m: int, group=None):
     return dict(works=works, recv=recv, bufs=bufs, P=P, m=m, group=group, chunk=chunk, lo=lo, hi=hi, d=d, dev=dev)
 
 
-def ordered_merge_finish(h) -> torch.Tensor:
+def ordered_merge_finish(h, summer=None) -> torch.Tensor:
     """Finish a merge: sum this rank's shard over micro-batches 0..m-1 in
     ascending order (ordered_sum, bit-identical to the sequential replay) and
-    all-gather the merged shards into the full gradient."""
-    from .optim import ordered_sum
+    all-gather the merged shards into the full gradient.  `summer(parts, out)`
+    replaces the device ordered_sum only in the CPU (gloo) tests of this
+    bookkeeping, which pass the oracle's sum."""
     import torch.distributed as dist
+    if summer is None:
+        from .optim import ordered_sum as summer
     for w in h["works"]:
         w.wait()
     lo, hi, chunk, d = h["lo"], h["hi"], h["chunk"], h["d"]
     shard = torch.zeros(chunk, dtype=torch.float32, device=h["dev"])
     if hi > lo:
         parts = [h["recv"][mb] if mb in h["recv"] else h["bufs"][mb][lo:hi] for mb in range(h["m"])]
-        ordered_sum(parts, out=shard[:hi - lo])
-    full = torch.empty(chunk * d, dtype=torch.float32, device=h["dev"])
-    dist.all_gather_into_tensor(full, shard, group=h["group"])
+        summer(parts, out=shard[:hi - lo])
+    if dist.get_backend(h["group"]) == "nccl":
+        full = torch.empty(chunk * d, dtype=torch.float32, device=h["dev"])
+        dist.all_gather_into_tensor(full, shard, group=h["group"])
+    else:  # gloo (CPU tests): list form
+        parts = [torch.empty_like(shard) for _ in range(d)]
+        dist.all_gather(parts, shard, group=h["group"])
+        full = torch.cat(parts)
     return full[:h["P"]]
 
 

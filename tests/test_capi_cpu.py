@@ -196,3 +196,16 @@ def test_state_create_rejects_zero_extent_and_overflow():
         st = LIB.rw_state_create(C.byref(out), 1, C.c_void_p(base), C.c_void_p(base), None, None, None, 32,
                                  arr, len(groups), 0)
         assert LIB.rw_status_name(st).decode() == "InvalidShape"
+
+
+def test_resolver_empty_rank_is_identity():
+    """A replacement with no state (n == 0) reports the identities of MIN / MAX
+    (t_min = UINT64_MAX, t_max = 0), so a C++ host that all-reduces the raw
+    summaries never drags the consensus to 0."""
+    h = OptimizerHyper(kind=2).to_c()
+    s = rw_resolve_summary()
+    check(LIB.rw_resolve_summarize(None, 0, None, C.byref(h), 2**64 - 1, C.byref(s)))
+    assert s.t_min == 2**64 - 1 and s.t_max == 0
+    assert s.undo_elems == s.redo_elems == s.redo_blocked == 0
+    # survivors at 10 / 11 plus an empty replacement -> the survivors' consensus
+    assert _c_resolve([[(10, 0), (11, 1)], []], [[False, False], []])[:2] == ("Undo", 10)

@@ -62,7 +62,7 @@ def test_fp64_bitexact_vs_reference_golden(golden, name):
     st.check_finite()
     assert st.markers() == [(blk["t0"] + 1, 1)]
     assert np.array_equal(_bits(_get(st, "x", 0)), _bits([F(s) for s in blk["step"]["x"]]))
-    assert np.array_equal(_get(st, "g", 0), np.array(g))  # block.g = grad (optim.cpp:349)
+    assert np.array_equal(_get(st, "g", 0), np.array(g))  # block.g = grad (optim.cpp:271)
     if kind != SGD:
         assert np.array_equal(_bits(_get(st, "m", 0)), _bits([F(s) for s in blk["step"]["m"]]))
     if kind in (ADAM, ADAMW):

@@ -186,3 +186,53 @@ def test_pipelined_transfer_world3():
         assert torch.equal(res[r]["x"], res[0]["x"]) and torch.equal(res[r]["v"], res[0]["v"])
         assert res[r]["mk"] == [(4, 0)] * 6 and res[r]["used"] == "pipelined"
     assert res[0]["nbytes"] == 41 * 4 * 3
+
+
+# ---- parallel recovery bookkeeping over gloo ----
+def _oracle_sum(parts, out):
+    """ordered_sum restated on the host (tensor.cpp:105-117: ((t0 + t1) + t2)
+    + ..., one fp32 rounding per add) -- the oracle stands in for the device
+    kernel so only the ownership / order / gather bookkeeping is under test."""
+    import numpy as np
+    acc = parts[0].numpy().astype(np.float32).copy()
+    for p in parts[1:]:
+        acc = (acc + p.numpy().astype(np.float32)).astype(np.float32)
+    out.copy_(torch.from_numpy(acc))
+
+
+def _mb_grad(mb, P):
+    g = torch.Generator().manual_seed(1000 + mb)
+    return torch.randn(P, generator=g) * (10.0 ** (mb % 3 - 1))  # mixed magnitudes: order matters
+
+
+def scen_ordered_merge(rank):
+    from paper_2302_06173_b200.replay import ordered_merge_finish, ordered_merge_start, parallel_assignment
+    world = dist.get_world_size()
+    out = {}
+    for P, m in ((1000, 4), (77, 5), (130, 1), (5, 3)):  # ragged P: empty / short shards; helpers without mbs
+        mine = parallel_assignment(m, world)[rank]
+        bufs = {mb: _mb_grad(mb, P) for mb in mine}
+        h = ordered_merge_start(bufs, P, m, device=torch.device("cpu"))
+        out[(P, m)] = (ordered_merge_finish(h, summer=_oracle_sum), mine)
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ordered_merge_bookkeeping_gloo(world):
+    """Every helper ends with the ascending-mb ordered sum of ALL micro-batches'
+    gradients, bit for bit equal to the sequential sum, and helper h owned
+    exactly {mb : mb mod d == h} (Fig 6: {0,2} / {1,3})."""
+    import numpy as np
+    res = _run(scen_ordered_merge, world=world)
+    for (P, m), _ in res[0].items():
+        exp = _mb_grad(0, P).numpy().astype(np.float32)
+        for mb in range(1, m):
+            exp = (exp + _mb_grad(mb, P).numpy().astype(np.float32)).astype(np.float32)
+        owned = sorted(mb for r in range(world) for mb in res[r][(P, m)][1])
+        assert owned == list(range(m))
+        for r in range(world):
+            got, mine = res[r][(P, m)]
+            assert mine == [mb for mb in range(m) if mb % world == r]
+            assert np.array_equal(got.numpy().view(np.uint32), exp.view(np.uint32)), (P, m, r)
+    if world == 2:
+        assert res[0][(1000, 4)][1] == [0, 2] and res[1][(1000, 4)][1] == [1, 3]
