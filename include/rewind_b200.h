@@ -123,6 +123,7 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
                     int32_t device);
 void rw_state_destroy(rw_state* s);
 uint32_t rw_state_num_groups(const rw_state* s);
+int rw_state_info(const rw_state* s, int32_t* dtype, uint64_t* total, int32_t* device);
 /* Behaviour flags of a state (default 0).
  * RW_STATE_LAMB_SEQUENTIAL_NORMS: the LAMB step forms ||x|| and ||update|| in
  *   the reference's left-to-right order (optim.cpp:199-208, one thread per
@@ -271,6 +272,97 @@ int rw_resolve_summarize(const rw_group* groups, uint32_t n, const uint8_t* grad
 int rw_resolve_plan(const rw_resolve_summary* global, int32_t policy, const rw_group* groups,
                     uint32_t n, uint8_t* actions, uint64_t* target, int32_t* strategy);
 
+/* ---- C++ recovery host over NCCL (recovery.cpp is absent) ----
+ * The orchestration a C++ training system links in place of the reference's
+ * missing recovery module: an NCCL communicator wrapper (nonblocking, so a
+ * dead peer never wedges a host thread), the resolver's exchange, apply_undo,
+ * replica recovery, the ordered merge of parallel recovery, and NCCL-native
+ * failure detection and repair.  Every collective
+ * runs on the communicator's own stream, ordered after the caller's `stream`
+ * and back.  NCCL failures return RW_CHANNEL_BROKEN (the reference's
+ * "detection signal"). */
+typedef struct rw_comm rw_comm;
+/* 128-byte ncclUniqueId (ncclGetUniqueId) for rw_comm_init, shared out of band */
+int rw_nccl_unique_id(void* id_out);
+/* ncclCommInitRankConfig with blocking = 0 on `device` */
+int rw_comm_init(rw_comm** out, const void* unique_id, int32_t nranks, int32_t rank, int32_t device);
+/* wrap an existing ncclComm_t (not owned: destroy leaves it alone) */
+int rw_comm_from_nccl(rw_comm** out, void* nccl_comm);
+int32_t rw_comm_rank(const rw_comm* c);
+int32_t rw_comm_size(const rw_comm* c);
+void* rw_comm_stream(rw_comm* c);   /* cudaStream_t the collectives run on */
+void* rw_comm_nccl(rw_comm* c);     /* the ncclComm_t */
+int rw_comm_destroy(rw_comm* c);    /* finalize + destroy (abort if the comm failed) */
+int rw_comm_abort(rw_comm* c);      /* ncclCommAbort + free */
+
+/* Failure detection: a thread polls ncclCommGetAsyncError every
+ * poll_us and watches every collective this library enqueued; one that has
+ * not completed after timeout_ms (0 = no timeout) marks the communicator
+ * failed (fail-stop: the peer is gone).  Host waits inside the library then
+ * return RW_CHANNEL_BROKEN instead of blocking. */
+enum { RW_COMM_OK = 0, RW_COMM_FAILED_NCCL_ERROR = 1, RW_COMM_FAILED_TIMEOUT = 2 };
+int rw_comm_watch(rw_comm* c, uint32_t poll_us, uint32_t timeout_ms);
+/* reason = RW_COMM_*; detect_ms = age of the stuck collective when detected */
+int rw_comm_failed(rw_comm* c, int32_t* reason, double* detect_ms);
+/* Repair among the survivors (collective over them): ncclCommShrink excluding
+ * the dead ranks, with NCCL_SHRINK_ABORT when `c` failed (its stuck kernels
+ * are terminated first).  The parent is then released with rw_comm_abort. */
+int rw_comm_shrink(rw_comm* c, const int32_t* exclude, int32_t n_exclude, rw_comm** out);
+
+/* Heartbeat membership (the global key-value store of SPEC:253-261, here a
+ * node-local shared file of per-rank CLOCK_MONOTONIC timestamps): rank r's
+ * thread stamps slot r every beat_us (rank -1 = observer); dead() lists ranks
+ * silent for more than timeout_ms (fail-stop).  A replacement opening a dead
+ * rank's slot revives it. */
+typedef struct rw_membership rw_membership;
+int rw_membership_open(rw_membership** out, const char* path, int32_t rank, int32_t nranks, uint32_t beat_us);
+int rw_membership_dead(rw_membership* m, uint32_t timeout_ms, int32_t* dead, int32_t cap, int32_t* n_dead);
+int rw_membership_close(rw_membership* m);
+
+/* consensus_iteration + per-group plan over the communicator:
+ * reads s's markers (s == NULL: a replacement with no state yet, which joins
+ * the exchange with the MIN/MAX identities), two exchanges (t_min MIN / t_max
+ * MAX, then costs MAX), then rw_resolve_plan.  actions: rw_state_num_groups(s)
+ * entries (RW_ACT_*). */
+typedef struct rw_resolution {
+  int32_t strategy;   /* RW_STRATEGY_* */
+  uint32_t n_undo;    /* local groups to undo / redo */
+  uint32_t n_redo;
+  uint32_t _pad;
+  uint64_t target;    /* consensus iteration after repair */
+  uint64_t t_min, t_max;
+} rw_resolution;
+int rw_resolve(rw_state* s, const rw_hyper* h, rw_comm* c, int32_t policy, const uint8_t* grad_ready,
+               uint8_t* actions, rw_resolution* out, void* stream);
+/* apply_undo / redo: re-arms flags cleared at iteration end
+ * (the decision is on t), undoes in reverse update order, or steps the
+ * lagging groups with the synchronised gradient `grad` (redo).  Update order
+ * is reverse layer order = descending group index. */
+int rw_apply_resolution(rw_state* s, const rw_hyper* h, const uint8_t* actions, int32_t strategy, const void* grad,
+                        void* stream);
+/* apply_undo + recover_replication as one pipeline: the root
+ * (the survivor) undoes its groups in `pieces` contiguous runs (0 = 16) on
+ * `stream` while the communicator stream broadcasts each resolved run of x,
+ * m, v (and g with RW_RECOVER_INCLUDE_GRAD) to every other rank; markers and
+ * LAMB trust stacks follow.  Every rank passes its own state of the same
+ * layout; non-roots pass actions = NULL.  *bytes_out = bytes per replacement. */
+enum { RW_RECOVER_INCLUDE_GRAD = 1 };
+int rw_recover_replication(rw_state* s, const rw_hyper* h, rw_comm* c, int32_t root, const uint8_t* actions,
+                           int32_t strategy, uint32_t flags, uint32_t pieces, void* stream, uint64_t* bytes_out);
+
+/* Ordered merge of parallel recovery: parts[mb] =
+ * this rank's fp32 partial gradient of micro-batch mb (n elements) for every
+ * mb with mb % nranks == rank (others NULL).  Rank j owns shard j (chunk =
+ * rw_ordered_reduce_chunk elements), receives every partial's shard j, sums
+ * them in ascending mb order (ordered_sum: bit-identical to the sequential
+ * replay) and the shards are all-gathered: `out` (rw_ordered_reduce_out_elems
+ * elements; the first n are the merged gradient) is the same on every rank. */
+uint64_t rw_ordered_reduce_chunk(uint64_t n, int32_t nranks);
+uint64_t rw_ordered_reduce_out_elems(uint64_t n, int32_t nranks);
+uint64_t rw_ordered_reduce_scratch_elems(uint64_t n, uint32_t m, int32_t nranks, int32_t rank);
+int rw_ordered_reduce(rw_comm* c, const float* const* parts, uint32_t m, uint64_t n, float* out, float* scratch,
+                      uint64_t scratch_elems, void* stream);
+
 /* ---- numerics ---- */
 /* seeded_fill(shape, seed) (tensor.cpp:94-103) on the device, bit-identical to
  * the host (fp64) / its single rounding (fp32).  offset = first counter index. */
@@ -356,6 +448,48 @@ int rw_mse_grad(const void* pred_bf16, const float* target, uint64_t n, uint64_t
                 void* grad_bf16, double* loss, double* scratch, void* stream);
 /* fp32 -> bf16 (weight shadows after an optimizer step) */
 int rw_cast_f32_to_bf16(const float* in, void* out, uint64_t n, void* stream);
+
+/* ---- replay drivers in C++  ----
+ * One stage of the replayed group: its descriptor (bf16 weight shadows w[l],
+ * fp32 biases b[l] = the master x of the bias blocks), its fp32 master state
+ * (blocks W0, b0, W1, b1, ... in blocks() order, model.cpp:12-20) and a flat
+ * fp32 gradient buffer in the state's layout. */
+typedef struct rw_replay_stage {
+  rw_stage_desc desc;
+  rw_state* state;
+  float* grad;
+} rw_replay_stage;
+/* The group's inbound log, one entry per (iteration - it0) * micro_batches + mb
+ * in timestamp order: activations entering its first stage (bf16 [rows,
+ * dims_in]) and gradients entering its last stage (bf16 [rows, dims_out]),
+ * device pointers.  acts == NULL: the group starts the pipeline and the inputs
+ * are re-derived (synth_inputs, model.cpp:190-193); grads == NULL: it ends the
+ * pipeline and the gradient is mse_loss against synth_targets (:174-198).  A
+ * NULL entry is MissingLogData. */
+typedef struct rw_replay_log {
+  const void* const* acts;
+  const void* const* grads;
+  uint64_t seed;
+} rw_replay_log;
+/* device workspace both drivers need (comm == NULL: rw_replay_group) */
+uint64_t rw_replay_workspace_bytes(const rw_replay_stage* stages, uint32_t n_stages, int64_t rows,
+                                   uint32_t micro_batches, rw_comm* comm);
+/* recover_replay: the group's checkpoint is already loaded in
+ * the stage states; iterations [it0, it1) are re-executed from the log: every
+ * micro-batch forward + backward in timestamp order, gradients accumulated in
+ * ascending micro-batch order (accumulate_grads), then one step of every
+ * block in reverse layer order, the flag clear and the shadow refresh.  Equal
+ * to the failure-free run bit for bit. */
+int rw_replay_group(const rw_replay_stage* stages, uint32_t n_stages, int64_t rows, uint32_t micro_batches,
+                    uint64_t it0, uint64_t it1, const rw_hyper* h, const rw_replay_log* log, void* workspace,
+                    uint64_t workspace_bytes, void* stream);
+/* recover_parallel for this helper (rank of `comm`, d = its
+ * size): micro-batches {mb : mb mod d == rank} each into its own
+ * partial gradients, rw_ordered_reduce per stage (ascending mb), the
+ * same step on every helper.  Bit-identical to rw_replay_group. */
+int rw_recover_parallel(const rw_replay_stage* stages, uint32_t n_stages, int64_t rows, uint32_t micro_batches,
+                        uint64_t it0, uint64_t it1, const rw_hyper* h, const rw_replay_log* log, rw_comm* comm,
+                        void* workspace, uint64_t workspace_bytes, void* stream);
 
 /* ---- logging capture path (logstore.cpp missing) ----
  * Upstream-backup log of inter-machine boundary tensors.  rw_logger_log never

@@ -457,6 +457,14 @@ int rw_state_set_flags(rw_state* s, uint32_t flags) {
   return RW_OK;
 }
 
+int rw_state_info(const rw_state* s, int32_t* dtype, uint64_t* total, int32_t* device) {
+  if (!s) return fail(RW_INVALID_ARGUMENT, "null state");
+  if (dtype) *dtype = s->dtype;
+  if (total) *total = s->total;
+  if (device) *device = s->device;
+  return RW_OK;
+}
+
 uint32_t rw_state_num_groups(const rw_state* s) { return s ? static_cast<uint32_t>(s->mirror.size()) : 0; }
 
 void* rw_state_ptr(rw_state* s, int which) {
