@@ -520,7 +520,7 @@ def config1_crash(reps: int = 40) -> dict:
     for i, t in enumerate((st.x, st.g, st.m)):
         seeded_fill_(t, 40 + i)
     h = OptimizerHyper(kind=SGDM, lr=0.1, momentum=0.9, dampening=0.0, weight_decay=1e-4)
-    dev_ms, wall_ms = [], []
+    dev_ms, idle_ms, wall_ms = [], [], []
     for r in range(reps + 3):
         st.write_markers([(10, 0)] * G)
         st.step(h, stop_after=G // 2)                      # crash mid-update
@@ -536,11 +536,23 @@ def config1_crash(reps: int = 40) -> dict:
         order = [i for i in reversed(st.update_order()) if i in set(plan.undo_ids)]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        st.undo(h, order)                                  # the undo launch alone, device time
+        st.undo(h, order)                                  # the undo call on an idle GPU
         e1.record()
         torch.cuda.synchronize()
+        # the same call queued behind a ~0.5 ms spin, so the host-side
+        # preparation (Python, ctypes, work list) overlaps the GPU: the
+        # device-visible cost of the call (metadata copy, launch, kernel)
+        st.write_markers([(10, 0)] * G)
+        st.step(h, stop_after=G // 2)
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(1_000_000)
+        f0.record()
+        st.undo(h, order)
+        f1.record()
+        torch.cuda.synchronize()
         if r >= 3:
-            dev_ms.append(e0.elapsed_time(e1))
+            idle_ms.append(e0.elapsed_time(e1))
+            dev_ms.append(f0.elapsed_time(f1))
     # the undo kernel alone (CUPTI activity record; the event-bracketed time
     # above also contains the host-side preparation of the launch)
     # (median of 25 crash/undo cycles; >= 20 runs for us-scale kernels)
@@ -562,6 +574,7 @@ def config1_crash(reps: int = 40) -> dict:
     out = dict(workload="config 1: SGDM 10M flat fp32, 100 groups, crash after 50 (MidUpdate(50)), resolve + "
                         "undo of the 50 updated groups",
                undo_groups=G // 2, undo_params=undo_params, undo_call_device_ms=round(dm, 4),
+               undo_call_idle_gpu_ms=round(statistics.median(idle_ms), 4),
                undo_kernel_us=round(kus[0], 1) if kus else None, undo_kernel_samples=25,
                undo_kernel_gbs=round(undo_params * 20 / (kus[0] * 1e-6) / 1e9, 1) if kus else None,
                roofline_us=round(undo_params * 20 / (_peaks()["hbm_gbs"] * 1e9) * 1e6, 1),

@@ -121,6 +121,12 @@ int rw_lr_at(const rw_hyper* h, uint64_t t, double* out);
 int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v,
                     void* vmax, uint64_t total, const rw_group* groups, uint32_t n_groups,
                     int32_t device);
+/* A state for a HOST-resident replica (CPU offload, larger than HBM): the
+ * group layout and the device marker table, no device x, g, m, v.  Only
+ * rw_optimizer_undo_host and the marker calls operate on it; step / undo /
+ * push calls fail with RW_INVALID_ARGUMENT. */
+int rw_state_create_host(rw_state** out, int32_t dtype, uint64_t total, const rw_group* groups,
+                         uint32_t n_groups, int32_t device);
 void rw_state_destroy(rw_state* s);
 uint32_t rw_state_num_groups(const rw_state* s);
 int rw_state_info(const rw_state* s, int32_t* dtype, uint64_t* total, int32_t* device);
@@ -183,13 +189,14 @@ int rw_optimizer_undo(rw_state* s, const rw_hyper* h, const uint32_t* group_ids,
 
 /* optimizer_undo for a state that lives in HOST memory in the same flat
  * layout (e.g. a CPU-offloaded replica): x, g, m, v are read from hx.. and
- * the undone x, m, v written to ox.. (may alias the inputs); the device
- * buffers of `s` are the staging area and end up holding the same result.
- * Groups are cut into slices of ~slice_elems elements (0 = 16M) in layout
- * order, tiling the span from the first to the last selected group (other
- * groups inside the span pass through unchanged; nothing outside it is
- * touched); per slice H2D, undo and D2H run on three streams as a pipeline, so
- * both PCIe directions overlap the kernel.  Host buffers must be pinned for
+ * the undone x, m, v written to ox.. (may alias the inputs; when they do not,
+ * groups that are not undone are copied through, so ox.. always receive the
+ * whole resolved state).  Groups are cut into slices of ~slice_elems elements
+ * (0 = 16M) in layout order; per slice H2D, undo and D2H run on three streams
+ * as a pipeline through a ring of three device staging slices owned by `s`,
+ * so both PCIe directions overlap the kernel and the device memory used is
+ * bounded by three slices however large the host state is (the device
+ * buffers of `s`, if any, are not touched).  Host buffers must be pinned for
  * the copies to be asynchronous.  Guards and markers exactly as
  * rw_optimizer_undo; ordered on `stream` (complete when it completes). */
 int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* group_ids, uint32_t n,

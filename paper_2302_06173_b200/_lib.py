@@ -83,6 +83,7 @@ def _load() -> C.CDLL:
         "rw_hyper_validate": (C.c_int, [P(rw_hyper)]),
         "rw_lr_at": (C.c_int, [P(rw_hyper), u64, P(dbl)]),
         "rw_state_create": (C.c_int, [P(vp), i32, vp, vp, vp, vp, vp, u64, P(rw_group), u32, i32]),
+        "rw_state_create_host": (C.c_int, [P(vp), i32, u64, P(rw_group), u32, i32]),
         "rw_state_destroy": (None, [vp]),
         "rw_state_num_groups": (u32, [vp]),
         "rw_state_read_groups": (C.c_int, [vp, P(rw_group), vp]),

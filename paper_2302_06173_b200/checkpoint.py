@@ -101,6 +101,13 @@ def write_checkpoint(states, ckpt_dir: str, iteration: int, worker: int | None =
         check(LIB.rw_ckpt_commit(ckpt_dir.encode(), iteration, 1))
 
 
+def commit_checkpoint(ckpt_dir: str, iteration: int, workers: int) -> None:
+    """Publish MANIFEST_<iteration> once every one of `workers` workers has
+    written its blobs (write_checkpoint(..., commit=False) per worker): the
+    global checkpoint becomes visible atomically."""
+    check(LIB.rw_ckpt_commit(ckpt_dir.encode(), iteration, workers))
+
+
 def latest_checkpoint(ckpt_dir: str) -> int:
     """Highest committed iteration (NoCheckpoint if none)."""
     it = C.c_uint64()

@@ -38,6 +38,16 @@ struct Uniform {
   double wd, mu, one_m_damp, b1, b2, one_m_b1, one_m_b2, eps;
 };
 
+// Small calls carry their work list and scalar sets in the kernel's
+// parameter space (__grid_constant__) instead of a pinned H2D copy: no copy
+// on the stream ahead of the kernel, so a 50-group undo costs one launch.
+constexpr uint32_t kInlineItems = 128;
+constexpr uint32_t kInlineSets = 16;
+struct InlineMeta {
+  WorkItem work[kInlineItems];
+  ScalarSet sets[kInlineSets];
+};
+
 struct LaunchArgs {
   int dtype;     // RW_F32 / RW_F64
   int kind;      // RW_SGD..RW_AMSGRAD
@@ -61,6 +71,9 @@ struct LaunchArgs {
   void* pg = nullptr;
   void* pm = nullptr;
   void* pv = nullptr;
+  // work == nullptr: the work list and sets are in *inl (host memory, copied
+  // into the launch's parameters)
+  const InlineMeta* inl = nullptr;
 };
 
 // One-time per-device setup of a call site (kernel attributes such as the

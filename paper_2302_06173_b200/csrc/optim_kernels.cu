@@ -46,7 +46,11 @@ struct Arith<float> {
   __device__ __forceinline__ static float mul(float a, float b) { return __fmul_rn(a, b); }
   __device__ __forceinline__ static float add(float a, float b) { return __fadd_rn(a, b); }
   __device__ __forceinline__ static float sub(float a, float b) { return __fsub_rn(a, b); }
+#ifdef RW_OPTIM_PROBE_NODIV  // probe only (wrong math): how much do the IEEE divides cost?
+  __device__ __forceinline__ static float div(float a, float b) { return __fmul_rn(a, b); }
+#else
   __device__ __forceinline__ static float div(float a, float b) { return __fdiv_rn(a, b); }
+#endif
   __device__ __forceinline__ static float sqrt(float a) { return __fsqrt_rn(a); }
   __device__ __forceinline__ static bool nonfinite(float a) {
     return (__float_as_uint(a) & 0x7f800000u) == 0x7f800000u;
@@ -215,21 +219,58 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, uint32_t 
                "r"(smem_u32(src)), "r"(bytes)
                : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy)
+__device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store_hint(void* dst, const void* src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
+// ... only until their shared-memory sources have been read (the stage can be
+// refilled; the global writes may still be in flight)
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-constexpr int kThreads = 256;
+#ifndef RW_OPTIM_THREADS
+#define RW_OPTIM_THREADS 256
+#endif
+constexpr int kThreads = RW_OPTIM_THREADS;
 #ifndef RW_OPTIM_STAGES
 #define RW_OPTIM_STAGES 3
 #endif
 #ifndef RW_OPTIM_SLOT_BYTES
 #define RW_OPTIM_SLOT_BYTES 8192
+#endif
+#ifndef RW_OPTIM_WAIT_READ
+#define RW_OPTIM_WAIT_READ 0
+#endif
+#ifndef RW_OPTIM_INTERLEAVE
+#define RW_OPTIM_INTERLEAVE 0
+#endif
+#ifndef RW_OPTIM_L2HINT
+#define RW_OPTIM_L2HINT 0
 #endif
 #ifndef RW_OPTIM_MIN_BLOCKS
 #define RW_OPTIM_MIN_BLOCKS 1
@@ -276,7 +317,11 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
     T* __restrict__ vmax, const T* __restrict__ grad, const WorkItem* __restrict__ work,
     uint32_t n_work, uint32_t total_chunks, const ScalarSet* __restrict__ sets, Uniform u,
     rw_group* __restrict__ groups, uint32_t* __restrict__ done, T* __restrict__ px,
-    T* __restrict__ pg, T* __restrict__ pm, T* __restrict__ pv) {
+    T* __restrict__ pg, T* __restrict__ pm, T* __restrict__ pv, const __grid_constant__ InlineMeta inl) {
+  if (work == nullptr) {  // small call: metadata in the parameter space
+    work = inl.work;
+    sets = inl.sets;
+  }
   using A = Arith<T>;
   using V = typename A::V;
   constexpr int EV = A::EV;
@@ -305,12 +350,20 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
   s.omb2 = A::cvt(u.one_m_b2);
   s.eps = A::cvt(u.eps);
 
-  // Each CTA owns a contiguous range of chunks, so the producer walks the
+  // The chunks a CTA visits increase monotonically, so the producer walks the
   // work list with a cursor and only touches global metadata when it
-  // crosses into the next group.
+  // crosses into the next group.  Contiguous: each CTA owns one range of
+  // chunks.  Interleaved: CTA b visits b, b + grid, b + 2 grid, ... so the
+  // whole grid sweeps one compact window of every stream at a time.
+#if RW_OPTIM_INTERLEAVE
+  const uint32_t n_mine = total_chunks > blockIdx.x ? (total_chunks - blockIdx.x + gridDim.x - 1) / gridDim.x : 0u;
+  auto chunk_of = [&](uint32_t j) { return blockIdx.x + j * gridDim.x; };
+#else
   const uint32_t per_cta = (total_chunks + gridDim.x - 1) / gridDim.x;
   const uint32_t c_begin = min(total_chunks, blockIdx.x * per_cta);
-  const uint32_t c_end = min(total_chunks, c_begin + per_cta);
+  const uint32_t n_mine = min(total_chunks, c_begin + per_cta) - c_begin;
+  auto chunk_of = [&](uint32_t j) { return c_begin + j; };
+#endif
 
   // producer-only state (thread 0): cached current work item
   uint32_t cur = 0, cur_cb = 0, cur_nc = 0, cur_gid = 0, cur_flags = 0;
@@ -331,11 +384,12 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
   if (tid == 0) {
     for (int i = 0; i < S; ++i) mbar_init(&full[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (c_begin < c_end) {
+    if (n_mine) {
+      const uint32_t c0 = chunk_of(0);
       uint32_t lo = 0, hi = n_work;
       while (hi - lo > 1) {
         const uint32_t mid = (lo + hi) >> 1;
-        if (work[mid].chunk_begin <= c_begin) lo = mid;
+        if (work[mid].chunk_begin <= c0) lo = mid;
         else hi = mid;
       }
       load_item(lo);
@@ -343,6 +397,19 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
   }
   __syncthreads();
 
+  // L2 policy of the streaming traffic (build option RW_OPTIM_L2HINT:
+  // 1 = loads evict-first, 2 = loads and stores, 3 = stores only)
+#if RW_OPTIM_L2HINT
+  const uint64_t l2pol = policy_evict_first();
+#if RW_OPTIM_L2HINT <= 2
+  auto bulk_load = [&](void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    bulk_load_hint(dst, src, bytes, b, l2pol);
+  };
+#endif
+#if RW_OPTIM_L2HINT >= 2
+  auto bulk_store = [&](void* dst, const void* src, uint32_t bytes) { bulk_store_hint(dst, src, bytes, l2pol); };
+#endif
+#endif
   // producer (thread 0): locate the tile, publish its descriptor, arm the
   // stage barrier with the byte count and launch the bulk loads
   auto issue = [&](uint32_t chunk, int st) {
@@ -387,6 +454,9 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
       acc_cnt = 0;
       return;
     }
+#if RW_OPTIM_WAIT_READ
+    bulk_wait<0>();  // stages were recycled on read-out: the writes themselves must be complete
+#endif
     __threadfence();
     const uint32_t prev = atomicAdd(&done[acc_item], acc_cnt);
     if (prev + acc_cnt == it.nchunks) {
@@ -406,15 +476,13 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
   };
 
   if (tid == 0) {
-    for (int k = 0; k < S; ++k) {
-      const uint32_t c = c_begin + uint32_t(k);
-      if (c < c_end) issue(c, k);
-    }
+    for (int k = 0; k < S; ++k)
+      if (uint32_t(k) < n_mine) issue(chunk_of(uint32_t(k)), k);
   }
 
-  uint32_t ring_item[D], ring_chunk[D];  // the last D tiles (thread 0)
+  uint32_t ring_item[D];  // the last D tiles' work items (thread 0)
   uint32_t iter = 0;
-  for (uint32_t chunk = c_begin; chunk < c_end; ++chunk, ++iter) {
+  for (; iter < n_mine; ++iter) {
     const int st = static_cast<int>(iter % S);
     mbar_wait(&full[st], (iter / S) & 1u);
     const StageMeta& mt = meta[st];
@@ -528,14 +596,17 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
       if (mt.bad) atomicOr(&groups[mt.gid].flags, 1u);
       const uint32_t this_item = mt.item;
       if (iter >= uint32_t(D)) {
+#if RW_OPTIM_WAIT_READ
+        bulk_wait_read<D>();  // tile iter-D's stores have read their stage: refill it
+#else
         bulk_wait<D>();  // tile iter-D's stores are complete: its stage can be refilled
+#endif
         const uint32_t r = (iter - D) % D;
         account(ring_item[r]);
-        const uint32_t nc = ring_chunk[r] + uint32_t(S);
-        if (nc < c_end) issue(nc, static_cast<int>((iter - D) % S));
+        const uint32_t nj = iter - D + uint32_t(S);  // the stage's next tile
+        if (nj < n_mine) issue(chunk_of(nj), static_cast<int>((iter - D) % S));
       }
       ring_item[iter % D] = this_item;
-      ring_chunk[iter % D] = chunk;
     }
   }
   if (tid == 0 && iter > 0) {
@@ -544,6 +615,8 @@ __global__ void __launch_bounds__(kThreads, RW_OPTIM_MIN_BLOCKS) optim_kernel(
     flush();
   }
 }
+
+const InlineMeta kNoInline{};
 
 template <typename T, int KIND, bool UNDO, bool COPY_GRAD, bool PUSH = false>
 int launch_t(const LaunchArgs& a, cudaStream_t st) {
@@ -572,7 +645,7 @@ int launch_t(const LaunchArgs& a, cudaStream_t st) {
                                      static_cast<T*>(a.vmax), static_cast<const T*>(a.grad), a.work,
                                      a.n_work, a.total_chunks, a.sets, a.u, a.groups, a.done,
                                      static_cast<T*>(a.px), static_cast<T*>(a.pg), static_cast<T*>(a.pm),
-                                     static_cast<T*>(a.pv));
+                                     static_cast<T*>(a.pv), a.inl ? *a.inl : kNoInline);
   return static_cast<int>(cudaGetLastError());
 }
 
@@ -669,6 +742,7 @@ int grid_for(uint64_t n, int threads) {
 }  // namespace
 
 uint32_t chunk_elems_for(int dtype) { return kSlotBytes / (dtype == RW_F64 ? 8u : 4u); }
+
 
 int launch_optim(const LaunchArgs& a, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);

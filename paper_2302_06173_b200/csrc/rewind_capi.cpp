@@ -124,6 +124,11 @@ struct rw_state {
   cudaStream_t h2d = nullptr;
   cudaStream_t d2h = nullptr;
   std::vector<cudaEvent_t> evs;
+  // its staging ring: kHostRing slots of x, g, m, v slices (device memory
+  // of its own, so the host-resident state may exceed HBM)
+  void* ring[3][4] = {};
+  uint64_t ring_cap = 0;  // elements per buffer
+  bool host_resident = false;  // created by rw_state_create_host: no device x, g, m, v
 };
 
 namespace {
@@ -188,6 +193,9 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
                   const void* grad, const std::vector<double>& etas, void* stream,
                   const uint8_t* copy_only = nullptr, void* const* peers = nullptr) {
   if (n == 0) return RW_OK;
+  if (s->host_resident)
+    return fail(RW_INVALID_ARGUMENT, "state was created by rw_state_create_host: it has no device buffers "
+                                     "(use rw_optimizer_undo_host)");
   RW_CUDA(cudaSetDevice(s->device));
   Slot& sl = s->slots[s->next_slot];
   s->next_slot = (s->next_slot + 1) % kSlots;
@@ -232,8 +240,16 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
   }
   if (chunk > 0xFFFFFFF0ull) return fail(RW_TOO_LARGE, "TooLarge: too many chunks in one call");
   auto cs = static_cast<cudaStream_t>(stream);
+  // small non-LAMB calls: metadata in the kernel parameters, no H2D copy
+  const bool inline_meta = !lamb && n_items <= rwb::kInlineItems && n_sets <= rwb::kInlineSets;
+  rwb::InlineMeta im;
   if (n_items > 0) {
-    RW_CUDA(cudaMemcpyAsync(sl.d_buf, sl.h_buf, sl.meta_bytes, cudaMemcpyHostToDevice, cs));  // work + sets
+    if (inline_meta) {
+      std::memcpy(im.work, sl.h_work, sizeof(rwb::WorkItem) * n_items);
+      std::memcpy(im.sets, sl.h_sets, sizeof(rwb::ScalarSet) * n_sets);
+    } else {
+      RW_CUDA(cudaMemcpyAsync(sl.d_buf, sl.h_buf, sl.meta_bytes, cudaMemcpyHostToDevice, cs));  // work + sets
+    }
     if (lamb && !undo) {
       // step_lamb first pass over every group: m, v, both norms, trust
       if (s->partial_cap < chunk) {
@@ -267,6 +283,11 @@ int launch_groups(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t 
     a.u = uniform_of(h);
     a.groups = s->d_groups;
     a.done = sl.d_done;
+    if (inline_meta) {
+      a.work = nullptr;
+      a.sets = nullptr;
+      a.inl = &im;
+    }
     if (peers) {
       a.px = peers[0];
       a.pg = peers[1];
@@ -379,13 +400,14 @@ int rw_lr_at(const rw_hyper* h, uint64_t t, double* out) {
   return lr_at(h, t, out);
 }
 
-int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v, void* vmax,
-                    uint64_t total, const rw_group* groups, uint32_t n_groups, int32_t device) {
+static int state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v, void* vmax,
+                        uint64_t total, const rw_group* groups, uint32_t n_groups, int32_t device,
+                        bool host_resident) {
   rwb::DeviceScope dev_scope(device);
   if (!out) return fail(RW_INVALID_ARGUMENT, "null out");
   *out = nullptr;
   if (dtype != RW_F32 && dtype != RW_F64) return fail(RW_INVALID_ARGUMENT, "dtype must be RW_F32 or RW_F64");
-  if (!x || !g) return fail(RW_INVALID_ARGUMENT, "x and g are required");
+  if (!host_resident && (!x || !g)) return fail(RW_INVALID_ARGUMENT, "x and g are required");
   for (void* p : {x, g, m, v, vmax})
     if (p && (reinterpret_cast<uintptr_t>(p) & 15u))
       return fail(RW_INVALID_ARGUMENT, "state buffers must be 16-byte aligned");
@@ -409,6 +431,7 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
   s->m = m;
   s->v = v;
   s->vmax = vmax;
+  s->host_resident = host_resident;
   s->total = total;
   s->mirror.assign(groups, groups + n_groups);
   for (auto& gr : s->mirror) gr.flags = 0;
@@ -428,6 +451,17 @@ int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, vo
   return RW_OK;
 }
 
+int rw_state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m, void* v, void* vmax,
+                    uint64_t total, const rw_group* groups, uint32_t n_groups, int32_t device) {
+  return state_create(out, dtype, x, g, m, v, vmax, total, groups, n_groups, device, false);
+}
+
+int rw_state_create_host(rw_state** out, int32_t dtype, uint64_t total, const rw_group* groups,
+                         uint32_t n_groups, int32_t device) {
+  return state_create(out, dtype, nullptr, nullptr, nullptr, nullptr, nullptr, total, groups, n_groups, device,
+                      true);
+}
+
 void rw_state_destroy(rw_state* s) {
   rwb::DeviceScope dev_scope(s ? s->device : -1);
   if (!s) return;
@@ -441,6 +475,8 @@ void rw_state_destroy(rw_state* s) {
     cudaFree(sl.d_buf);
     cudaFree(sl.d_done);
   }
+  for (auto& r : s->ring)
+    for (void* p : r) cudaFree(p);
   cudaFree(s->d_groups);
   cudaFree(s->d_trust);
   cudaFree(s->d_partial);
@@ -668,8 +704,8 @@ int undo_prepare(rw_state* s, const rw_hyper* h, const uint32_t* ids, uint32_t n
       default: return fail(RW_INVALID_ARGUMENT, "unknown optimizer kind %d", h->kind);
     }
   }
-  if ((h->kind != RW_SGD && !s->m) ||
-      ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB) && !s->v))
+  if (!s->host_resident && ((h->kind != RW_SGD && !s->m) ||
+                            ((h->kind == RW_ADAM || h->kind == RW_ADAMW || h->kind == RW_LAMB) && !s->v)))
     return fail(RW_INVALID_ARGUMENT, "%s needs m/v buffers", kind_name(h->kind));
   if (h->kind == RW_LAMB) return lamb_undo_scalars(s, h, ids, n, etas, stream);
   return RW_OK;
@@ -731,6 +767,25 @@ int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, 
     sd.gids.push_back(ids[k]);
     sd.etas.push_back(etas[k]);
   }
+  // staging ring: slice k lives in slot k % kRing at offset 0 (its work
+  // items are slice-relative), so device memory is bounded by kRing slices
+  // whatever the size of the host-resident state
+  constexpr size_t kRing = 3;
+  uint64_t cap = 0;
+  for (const SliceDesc& sd : slices) cap = std::max<uint64_t>(cap, sd.end - sd.begin);
+  const size_t es = elem_size(s->dtype);
+  if (cap > s->ring_cap) {
+    RW_CUDA(cudaDeviceSynchronize());  // earlier calls may still read the old ring
+    for (auto& r : s->ring)
+      for (void*& q : r) {
+        cudaFree(q);
+        q = nullptr;
+      }
+    s->ring_cap = 0;
+    for (auto& r : s->ring)
+      for (void*& q : r) RW_CUDA(cudaMalloc(&q, cap * es));
+    s->ring_cap = cap;
+  }
   while (s->evs.size() < 3 * slices.size() + 1) {
     cudaEvent_t e;
     RW_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -763,7 +818,7 @@ int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, 
       const uint32_t sidx = lamb ? item : set_of[gr.t];
       sl.h_sets[sidx] = scalars_at(h, gr.t, slices[k].etas[j]);
       rwb::WorkItem& w = sl.h_work[item++];
-      w.off = gr.offset;
+      w.off = gr.offset - slices[k].begin;  // slice-relative: the ring slot holds the slice at 0
       w.len = gr.len;
       w.new_t = gr.t - 1;
       w.gid = gid;
@@ -778,33 +833,49 @@ int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, 
     chunks[k] = static_cast<uint32_t>(chunk);
   }
   RW_CUDA(cudaMemcpyAsync(sl.d_buf, sl.h_buf, sl.meta_bytes, cudaMemcpyHostToDevice, cs));  // work + sets
-  const size_t es = elem_size(s->dtype);
   cudaEvent_t start = s->evs[3 * slices.size()];
   RW_CUDA(cudaEventRecord(start, cs));  // prior work + the metadata upload first
   RW_CUDA(cudaStreamWaitEvent(s->h2d, start, 0));
   RW_CUDA(cudaStreamWaitEvent(s->d2h, start, 0));
   const void* hin[4] = {hx, hg, um ? hm : nullptr, uv ? hv : nullptr};
-  void* din[4] = {s->x, s->g, s->m, s->v};
   void* hout[3] = {ox, um ? om : nullptr, uv ? ov : nullptr};
-  void* dout[3] = {s->x, s->m, s->v};
+  // out != in: the parts of the layout outside the span pass through too
+  {
+    const uint64_t span_b = slices.front().begin, span_e = slices.back().end;
+    const int in_of_out[3] = {0, 2, 3};
+    for (int b = 0; b < 3; ++b) {
+      if (!hout[b] || hout[b] == hin[in_of_out[b]]) continue;
+      auto* o = static_cast<char*>(hout[b]);
+      auto* i = static_cast<const char*>(hin[in_of_out[b]]);
+      if (span_b) RW_CUDA(cudaMemcpyAsync(o, i, span_b * es, cudaMemcpyHostToHost, s->d2h));
+      if (span_e < s->total)
+        RW_CUDA(cudaMemcpyAsync(o + span_e * es, i + span_e * es, (s->total - span_e) * es, cudaMemcpyHostToHost,
+                                s->d2h));
+    }
+  }
   for (size_t k = 0; k < slices.size(); ++k) {
     const SliceDesc& sd = slices[k];
     const uint64_t off = sd.begin * es, bytes = (sd.end - sd.begin) * es;
+    void* const* slot_buf = s->ring[k % kRing];
+    void* din[4] = {slot_buf[0], slot_buf[1], slot_buf[2], slot_buf[3]};
+    void* dout[3] = {slot_buf[0], slot_buf[2], slot_buf[3]};
+    // the slot's previous slice must have left for the host before it is refilled
+    if (k >= kRing) RW_CUDA(cudaStreamWaitEvent(s->h2d, s->evs[3 * (k - kRing) + 2], 0));
     for (int b = 0; b < 4; ++b)
       if (hin[b])
-        RW_CUDA(cudaMemcpyAsync(static_cast<char*>(din[b]) + off, static_cast<const char*>(hin[b]) + off, bytes,
-                                cudaMemcpyHostToDevice, s->h2d));
+        RW_CUDA(cudaMemcpyAsync(din[b], static_cast<const char*>(hin[b]) + off, bytes, cudaMemcpyHostToDevice,
+                                s->h2d));
     RW_CUDA(cudaEventRecord(s->evs[3 * k], s->h2d));
     RW_CUDA(cudaStreamWaitEvent(cs, s->evs[3 * k], 0));
     rwb::LaunchArgs a;
     a.dtype = s->dtype;
     a.kind = h->kind;
     a.undo = true;
-    a.x = s->x;
-    a.g = s->g;
-    a.m = s->m;
-    a.v = s->v;
-    a.vmax = s->vmax;
+    a.x = din[0];
+    a.g = din[1];
+    a.m = din[2];
+    a.v = din[3];
+    a.vmax = nullptr;
     a.grad = nullptr;
     a.work = sl.d_work + first[k];
     a.n_work = static_cast<uint32_t>(sd.gids.size());
@@ -823,8 +894,7 @@ int rw_optimizer_undo_host(rw_state* s, const rw_hyper* h, const uint32_t* ids, 
     RW_CUDA(cudaStreamWaitEvent(s->d2h, s->evs[3 * k + 1], 0));
     for (int b = 0; b < 3; ++b)
       if (hout[b])
-        RW_CUDA(cudaMemcpyAsync(static_cast<char*>(hout[b]) + off, static_cast<const char*>(dout[b]) + off, bytes,
-                                cudaMemcpyDeviceToHost, s->d2h));
+        RW_CUDA(cudaMemcpyAsync(static_cast<char*>(hout[b]) + off, dout[b], bytes, cudaMemcpyDeviceToHost, s->d2h));
     RW_CUDA(cudaEventRecord(s->evs[3 * k + 2], s->d2h));
   }
   for (uint32_t i = 0; i < n; ++i) {  // host mirror follows the kernels' marker writes

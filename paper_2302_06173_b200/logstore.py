@@ -14,7 +14,7 @@ import collections
 import ctypes as C
 import glob
 import os
-from typing import Iterator
+from typing import Iterable, Iterator
 
 import torch
 
@@ -140,16 +140,23 @@ def read_chunk(path: str, max_payload: int = 1 << 30) -> Iterator[tuple[rw_log_r
         LIB.rw_log_close(h)
 
 
-def load_log_dir(directory: str, device=None, max_payload: int = 1 << 30, machine: int | None = None):
+def load_log_dir(directory: str, device=None, max_payload: int = 1 << 30, machine: int | None = None,
+                 receivers: Iterable[int] | None = None, min_iteration: int = 0):
     """fetch_logs for replay: every committed chunk file of the
-    directory (optionally one machine's), payloads moved to the device and
-    CRC-verified there.  Returns a replay.BoundaryLog."""
+    directory (optionally one sender machine's), keeping the records addressed
+    to `receivers` (the failed group's first and last stage: its inbound
+    activations and gradients; default all) from iteration `min_iteration` on,
+    payloads moved to the device and CRC-verified there.  Returns a
+    replay.BoundaryLog."""
     from .replay import BoundaryLog
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     pat = "m*.swft" if machine is None else f"m{machine:04d}_*.swft"
     log = BoundaryLog()
+    recv = None if receivers is None else set(int(x) for x in receivers)
     for path in sorted(glob.glob(os.path.join(directory, pat))):
         for r, payload in read_chunk(path, max_payload):
+            if (recv is not None and int(r.receiver) not in recv) or int(r.iteration) < min_iteration:
+                continue
             d = payload.to(dev, non_blocking=True)
             if crc32_device(d) != r.crc32:
                 raise RwError(15, f"CorruptLog: CRC mismatch in {path} (it {r.iteration}, mb {r.mb})")

@@ -115,7 +115,7 @@ class DeviceState:
     def __init__(self, sizes: Sequence[int], dtype: torch.dtype = torch.float32,
                  device: int | torch.device | None = None, kind: int = ADAM,
                  with_vmax: bool = False,
-                 align: int = ALIGN_ELEMS):
+                 align: int = ALIGN_ELEMS, host_resident: bool = False, stagger_bytes: int | None = None):
         if not torch.cuda.is_available():
             raise RwError(_lib.RW_CUDA_ERROR, "no CUDA device: the B200 path has no CPU fallback")
         if device is None:
@@ -131,17 +131,35 @@ class DeviceState:
         self.kind = kind
         uses_m = kind != SGD
         uses_v = kind in (ADAM, ADAMW, AMSGRAD, LAMB)
-        alloc = lambda: torch.zeros(max(self.total, 1), dtype=dtype, device=dev)  # noqa: E731
-        self.x = alloc()
-        self.g = alloc()
-        self.m = alloc() if uses_m else None
-        self.v = alloc() if uses_v else None
-        self.vmax = alloc() if (with_vmax or kind == AMSGRAD) else None
         groups = (rw_group * len(self.sizes))()
         for i, (o, n) in enumerate(zip(self.offsets, self.sizes)):
             groups[i].offset, groups[i].len, groups[i].t = o, n, 0
             groups[i].updated, groups[i].flags = 0, 0
         self._h = C.c_void_p()
+        self.host_resident = host_resident
+        if host_resident:  # layout + markers only: undo_from_host on host tensors (rw_state_create_host)
+            self.x = self.g = self.m = self.v = self.vmax = None
+            check(LIB.rw_state_create_host(C.byref(self._h), self.rw_dtype, self.total, groups,
+                                           len(self.sizes), dev.index or 0))
+            return
+        uses_w = with_vmax or kind == AMSGRAD
+        if stagger_bytes is None:
+            alloc = lambda: torch.zeros(max(self.total, 1), dtype=dtype, device=dev)  # noqa: E731
+        else:
+            # one slab, buffer k starting k x (buffer bytes + stagger) in: the
+            # streams the kernels read side by side (x[i], g[i], m[i], v[i])
+            # are not a power-of-two distance apart in the physical address space
+            es = torch.tensor([], dtype=dtype).element_size()
+            pitch = (max(self.total, 1) * es + int(stagger_bytes) + 255) // 256 * 256 // es
+            nbuf = 2 + int(uses_m) + int(uses_v) + int(uses_w)
+            self._slab = torch.zeros(pitch * nbuf, dtype=dtype, device=dev)
+            views = iter(self._slab[k * pitch:k * pitch + max(self.total, 1)] for k in range(nbuf))
+            alloc = lambda: next(views)  # noqa: E731
+        self.x = alloc()
+        self.g = alloc()
+        self.m = alloc() if uses_m else None
+        self.v = alloc() if uses_v else None
+        self.vmax = alloc() if uses_w else None
         ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
         check(LIB.rw_state_create(C.byref(self._h), self.rw_dtype, ptr(self.x), ptr(self.g),
                                   ptr(self.m), ptr(self.v), ptr(self.vmax), self.total, groups,

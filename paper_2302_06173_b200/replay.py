@@ -306,15 +306,28 @@ class Pipeline:
         self.iteration = 0
         self.losses: list[float] = []
 
-    def run_iteration(self, log_group: tuple[int, int] | None = None, log=None) -> float:
+    def run_iteration(self, log_group: tuple[int, int] | None = None, log=None,
+                      cuts: Sequence[int] | None = None, senders: dict | None = None) -> float:
         """One training iteration.  `log` is a BoundaryLog (in HBM / pinned) or a
         logstore.Logger (async D2H + SWFT chunk files); the messages into the
-        group [g0, g1] are logged at send time (upstream backup)."""
-        if log is not None and not isinstance(log, BoundaryLog):
-            return self._run_iteration(log_group, _LoggerSink(log))
-        return self._run_iteration(log_group, log)
+        group [g0, g1] are logged at send time (upstream backup).
 
-    def _run_iteration(self, log_group, log) -> float:
+        Machines: `cuts` lists the stages that begin a machine (stage s with a
+        machine boundary between s-1 and s); every message that crosses a cut
+        is logged by its SENDER's machine, senders[machine] being that
+        machine's Logger / BoundaryLog (each machine keeps the
+        messages it sent, so a failed machine's inbound traffic survives on
+        its neighbours)."""
+        wrap = lambda lg: lg if (lg is None or isinstance(lg, BoundaryLog)) else _LoggerSink(lg)  # noqa: E731
+        route = None
+        if cuts:
+            cut_set = sorted(set(int(c) for c in cuts))
+            machine_of = lambda st: sum(1 for c in cut_set if c <= st)  # noqa: E731
+            sinks = {k: wrap(v) for k, v in (senders or {}).items()}
+            route = (set(cut_set), machine_of, sinks)
+        return self._run_iteration(log_group, wrap(log), route)
+
+    def _run_iteration(self, log_group, log, route=None) -> float:
         it = self.iteration
         dev = self.stages[0].device
         loss = torch.zeros(1, dtype=torch.float64, device=dev)
@@ -326,6 +339,8 @@ class Pipeline:
                 acts = st.new_acts(self.rows, x)
                 if log_group and log is not None and s == log_group[0] and s > 0:
                     log.put("act", it, mb, x, sender=s - 1, receiver=s)
+                if route and s in route[0] and route[1](s - 1) in route[2]:
+                    route[2][route[1](s - 1)].put("act", it, mb, x, sender=s - 1, receiver=s)
                 x = st.forward(acts)
                 all_acts.append(acts)
             tgt = synth_targets(self.seed, it, mb, self.rows, self.dim, device=dev)
@@ -334,6 +349,8 @@ class Pipeline:
             for s in range(self.p - 1, -1, -1):
                 if log_group and log is not None and s == log_group[1] and s < self.p - 1:
                     log.put("grad", it, mb, g, sender=s + 1, receiver=s)
+                if route and (s + 1) in route[0] and route[1](s + 1) in route[2]:
+                    route[2][route[1](s + 1)].put("grad", it, mb, g, sender=s + 1, receiver=s)
                 gout = torch.empty(self.rows, self.dim, dtype=torch.bfloat16, device=dev) if s > 0 else None
                 self.stages[s].backward(all_acts[s], g, gout, accumulate=mb > 0)
                 g = gout

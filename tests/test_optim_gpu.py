@@ -274,12 +274,16 @@ def test_large_state_roundtrip_sampled(restate):
     assert ((st.x - x0).abs() <= 2 * torch.finfo(torch.float32).eps * sp + 1e-30).all()
 
 
+@pytest.mark.parametrize("ids", [[5, 3, 1, 0], [3, 1]])
 @pytest.mark.parametrize("kind,dtype", [(ADAM, torch.float32), (SGDM, torch.float32), (ADAM, torch.float64),
                                          ("lamb", torch.float32)])
-def test_undo_from_host_pipelined_equals_device_undo(kind, dtype):
-    """rw_optimizer_undo_host (H2D | undo | D2H pipelined per slice) gives the
-    same bits and markers as the device-resident undo, for many small slices;
-    LAMB's host-resident undo takes the saved trust ratios of the staging state."""
+def test_undo_from_host_pipelined_equals_device_undo(kind, dtype, ids):
+    """rw_optimizer_undo_host (H2D | undo | D2H pipelined per slice through a
+    three-slice device ring) gives the same bits and markers as the
+    device-resident undo, for many small slices, on a host-resident state
+    (rw_state_create_host: no device copy of x, g, m, v); groups not undone
+    reach `out` unchanged, inside and outside the span of the undone ones.
+    LAMB's host-resident undo takes the saved trust ratios of the state."""
     from paper_2302_06173_b200 import LAMB
     lamb = kind == "lamb"
     kind = LAMB if lamb else kind
@@ -295,27 +299,34 @@ def test_undo_from_host_pipelined_equals_device_undo(kind, dtype):
     ref.write_markers([(5, 0)] * len(sizes))
     ref.step(h)  # the pending update to undo (LAMB saves its trust ratios here)
     host = {k: getattr(ref, k).cpu().pin_memory() for k in ("x", "g", "m", "v") if getattr(ref, k) is not None}
-    st = DeviceState(sizes, dtype=dtype, kind=kind)
+    st = DeviceState(sizes, dtype=dtype, kind=kind, host_resident=True)
+    assert st.x is None
     st.write_markers(ref.markers())
     if lamb:
         for i in range(len(sizes)):
             st.set_saved_scalars(i, ref.saved_scalars(i))
     out = {k: torch.zeros_like(v).pin_memory() for k, v in host.items() if k != "g"}
-    ids = [5, 3, 1, 0]
     st.undo_from_host(h, host, out, ids=ids, slice_elems=2000)
     torch.cuda.synchronize()
     ref.undo(h, ids)
-    lo, hi = st.offsets[0], st.offsets[5] + sizes[5]  # the span first..last selected group
-    for k in out:
-        # undone groups: bit-exact vs device undo; groups 2, 4 pass through unchanged
-        assert torch.equal(out[k][lo:hi].cuda(), getattr(ref, k)[lo:hi]), k
-        assert torch.equal(getattr(st, k)[lo:hi], getattr(ref, k)[lo:hi]), k
+    for k in out:  # undone groups bit-exact vs the device undo, the rest passed through
+        assert torch.equal(out[k].cuda(), getattr(ref, k)), k
     assert st.markers() == ref.markers()
+    with pytest.raises(RwError) as e:  # no device buffers: device-resident calls refuse
+        st.undo(h, [2])
+    assert e.value.name == "InvalidArgument"
     if lamb:
         assert [len(st.saved_scalars(i)) for i in ids] == [0] * len(ids)
     with pytest.raises(RwError) as e:  # guards before any copy
-        st.undo_from_host(h, host, out, ids=[0])
+        st.undo_from_host(h, host, out, ids=[ids[-1]])
     assert e.value.name == "NothingToUndo"
+    if not lamb:  # a device-resident state's own buffers are not the staging area
+        dv = DeviceState(sizes, dtype=dtype, kind=kind)
+        dv.write_markers([(6, 1)] * len(sizes))
+        dv.undo_from_host(h, host, {k: torch.empty_like(v).pin_memory() for k, v in out.items()}, ids=ids,
+                          slice_elems=2000)
+        torch.cuda.synchronize()
+        assert float(dv.x.abs().sum()) == 0.0
 
 
 @pytest.mark.parametrize("cfg", ["adam340m", "adam1b"])
@@ -408,3 +419,4 @@ def test_empty_group_lists_are_noops():
     assert st.markers() == mk
     for k, t in before.items():
         assert torch.equal(getattr(st, k), t), k
+
