@@ -798,6 +798,8 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
                                                 recover_replication_fused, resolve)
     from paper_2302_06173_b200.workloads import gpt2_xl_sizes
     sizes = gpt2_xl_sizes()
+    nvl = nvlink_probe(world, rank, device) if world > 1 else None
+    nvl_bps = (nvl["copy_engine_gbs"] if nvl else 770.0) * 1e9
     st = DeviceState(sizes, kind=ADAM, device=device.index)
     h = OptimizerHyper(kind=ADAM, lr=1e-4, weight_decay=0.01)
     if rank == 0:
@@ -844,7 +846,7 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
                          strategy=res[0][1], target_iteration=res[0][2],
                          bytes_per_replacement=nbytes,
                          transfer_algbw_gbs=round(nbytes / (ms * 1e-3) / 1e9, 1) if nbytes else None,
-                         frac_of_nvlink_roofline=round(nbytes / 770e9 / (ms * 1e-3), 3) if nbytes else None)
+                         frac_of_nvlink_roofline=round(nbytes / nvl_bps / (ms * 1e-3), 3) if nbytes else None)
         if kinfo and "used" in kinfo[0]:
             out[mode]["transfer"] = kinfo[0]["used"]
         elif kinfo:
@@ -856,8 +858,48 @@ def recovery_e2e(world: int, rank: int, device, steps: int = 3):
     torch.cuda.empty_cache()
     out["workload"] = ("config 3: GPT-2 XL (1,557,611,200 params, 580 groups) Adam fp32; rank 0 crashed "
                        "after 290/580 groups; ranks 1..N-1 replacements; x, m, v = 18.7 GB per replacement")
-    out["nvlink_roofline_ms"] = round(18691334400 / 770e9 * 1e3, 2) if world > 1 else None
+    out["nvlink_roofline_ms"] = round(18691334400 / nvl_bps * 1e3, 2) if world > 1 else None
+    out["nvlink_probe"] = nvl
     return out
+
+
+def nvlink_probe(world: int, rank: int, device, nbytes: int = 2 << 30, reps: int = 5) -> dict:
+    """The replica transfer's roofline, measured in this run: rank 0 writes
+    `nbytes` into rank 1's HBM through CUDA IPC with the copy engines (the
+    engine the chain transfer uses), best of `reps`, CUDA events."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_06173_b200._lib import LIB, check
+    from paper_2302_06173_b200.recovery import _allgather_exports
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    ex = _allgather_exports([buf])
+    best = None
+    if rank == 0:
+        hb, off = ex[1][0]
+        base = C.c_void_p()
+        check(LIB.rw_ipc_import(hb, C.byref(base)))
+        s = torch.cuda.Stream(device=device)
+        dst = (C.c_void_p * 1)(base.value + off)
+        src = (C.c_void_p * 1)(buf.data_ptr())
+        nb = (C.c_uint64 * 1)(nbytes)
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            check(LIB.rw_copy_async(dst, src, nb, 1, C.c_void_p(s.cuda_stream)))
+            b.record(s)
+            b.synchronize()
+            ms = a.elapsed_time(b)
+            best = ms if best is None else min(best, ms)
+        LIB.rw_ipc_close(base)
+    dist.barrier()
+    t = torch.tensor([nbytes / (best * 1e-3) / 1e9 if best else 0.0], device=device)
+    dist.broadcast(t, 0)
+    del buf
+    return dict(copy_engine_gbs=round(float(t.item()), 1), bytes=nbytes,
+                how="rank 0 -> rank 1 HBM, cudaMemcpyAsync to a CUDA-IPC mapping, best of %d" % reps)
 
 
 def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 16384, m: int = 8,
