@@ -1250,6 +1250,14 @@ def _summarize(extras: dict) -> dict:
     return out
 
 
+# single-GPU extras runnable on their own (`bench.py --only NAME`)
+ONLY = {
+    "logging_capture": lambda: logging_bench(),
+    "config5_sweep": lambda: config5_sweep(),
+    "config1_crash": lambda: config1_crash(),
+}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1261,9 +1269,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-replay", action="store_true")
     ap.add_argument("--replay-iters", type=int, default=2)
+    ap.add_argument("--only", choices=sorted(ONLY), help="run one single-GPU extra and print its JSON")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3
+    if args.only:
+        print(json.dumps(ONLY[args.only](), indent=1))
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

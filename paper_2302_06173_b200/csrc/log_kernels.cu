@@ -6,13 +6,12 @@
 // CRC is affine over GF(2): with raw(M) the register after processing M from
 // state 0 and S^n the linear map "advance the register through n zero bytes",
 //   raw(A || B) = S^|B|(raw(A)) ^ raw(B),   crc(M) = ~(S^|M|(~0) ^ raw(M)).
-// Level 1: each CTA stages a 64 KB chunk in smem (coalesced 16-byte loads, one
-// padding word per 256-byte piece against bank conflicts), 256 threads compute
-// raw CRCs of 256-byte pieces 4 bytes at a time (slice-by-4 smem tables), and the
-// pieces are folded with a log-depth tree using S^256, S^512, ... operators.
-// Level 2: one thread folds the chunk CRCs with S^65536 and the tail, and
-// applies the init/xorout conditioning.  Operators are 32x32 GF(2) matrices
-// (32 uint32 columns) built on the host.
+// Level 1 (crc_chunks_kernel): 64 KB chunks, lane pieces of 128 bytes read
+// with 256-bit loads, slice-by-4 bank-sliced smem tables, shuffle + smem fold.
+// Level 2 (crc_final_kernel): one CTA folds the unit raws and the tail as
+// trees and applies the init/xorout conditioning.  Operators are 32x32 GF(2)
+// matrices (32 uint32 columns) built on the host, applied on the device by
+// bit loop or through byte tables.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -25,16 +24,18 @@
 namespace rwb {
 namespace {
 
-constexpr int kCrcThreads = 256;
-constexpr uint32_t kPiece = 256;                      // bytes per thread
-constexpr uint32_t kChunk = kPiece * kCrcThreads;     // 64 KB per CTA
-constexpr int kLevels = 8;                            // log2(256) tree levels
+constexpr uint32_t kPiece = 128;                        // bytes per lane
+constexpr uint32_t kChunk = 65536;                      // bytes per chunk (16 warps)
+constexpr int kWarpsPerChunk = int(kChunk / (kPiece * 32));  // 16
+constexpr int kLevels = 9;                              // S^(128 * 2^l): 5 in-warp + 4 across warps
+constexpr int kChunkThreads = 1024;                     // 2 chunks per CTA pass
+constexpr int kChunksPerPass = kChunkThreads / 32 / kWarpsPerChunk;
+constexpr int kFinThreads = 256;
+constexpr int kFinLevels = 8;                           // log2(256)
+constexpr uint32_t kTailPiece = kChunk / kFinThreads;   // 256 bytes per thread of the tail
 
 struct Mat {
   uint32_t c[32];
-};
-struct TreeOps {
-  Mat op[kLevels];  // S^(256 * 2^l)
 };
 
 __host__ __device__ inline uint32_t mat_apply(const Mat& m, uint32_t v) {
@@ -78,121 +79,199 @@ __host__ __device__ inline Mat op_pow(Mat base, uint64_t n) {  // S^n
   return r;
 }
 
-// smem layout of a staged chunk: piece t (256 bytes) at word t * kPieceWords,
-// one padding word per piece, so that thread t reading word k of its piece
-// hits bank (t + k) % 32 -- conflict free (an unpadded 256-byte stride puts
-// all 32 lanes in one bank)
-constexpr uint32_t kPieceWords = kPiece / 4 + 1;
-constexpr uint32_t kChunkSmem = kCrcThreads * kPieceWords * 4;
+struct TreeOps {
+  Mat op[kLevels];  // S^(128 * 2^l)
+};
 
-__global__ void __launch_bounds__(kCrcThreads) crc_chunks_kernel(const uint8_t* __restrict__ data, uint64_t n,
-                                                                 TreeOps ops, uint32_t* __restrict__ chunk_raw) {
-  __shared__ uint32_t table[4][256];  // slice-by-4
-  extern __shared__ __align__(16) uint32_t wbuf[];  // kChunkSmem bytes (dynamic, opt-in > 48 KB)
-  __shared__ uint32_t part[kCrcThreads];
-  const uint32_t t = threadIdx.x;
-  {
-    uint32_t e = crc_table_entry(t);
-    table[0][t] = e;
+// Level 1, persistent: one 1024-thread CTA per SM, two 64 KB chunks per pass
+// (16 warps per chunk; lane L of warp w owns the 128-byte piece 32 w + L).
+// A lane reads its piece straight from global memory with four 256-bit loads
+// (LDG.256), all issued before the first lookup.  The slice-by-4 tables are BANK-SLICED: entry b of
+// table k for lane L sits at word (k * 256 + b) * 32 + L, i.e. in bank L, so
+// a warp's 32 random lookups never conflict (a shared 256-entry table costs
+// ~3.5 wavefronts per lookup): 128 KB.  The pieces fold into the chunk's raw
+// CRC with S^(128 * 2^l) applied through byte tables (4 lookups each):
+// levels 0-4 by warp shuffles, 5-8 across the chunk's 16 warps.
+constexpr uint32_t kSliceWords = 4 * 256 * 32;
+constexpr uint32_t kOpWords = kLevels * 4 * 256;
+constexpr uint32_t kChunkSmem = (kSliceWords + kOpWords + kChunkThreads / 32) * 4;
+
+__device__ __forceinline__ uint32_t op_apply_tab(const uint32_t* ot, uint32_t v) {
+  return ot[v & 0xFFu] ^ ot[256 + ((v >> 8) & 0xFFu)] ^ ot[512 + ((v >> 16) & 0xFFu)] ^ ot[768 + (v >> 24)];
+}
+// byte tables of an operator: ot[j * 256 + b] = m(b << 8j)
+__device__ __forceinline__ uint32_t op_tab_entry(const Mat& m, uint32_t i) {
+  const uint32_t j = i >> 8, b = i & 0xFFu;
+  uint32_t r = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    if (b & (1u << q)) r ^= m.c[8 * j + q];
+  return r;
+}
+
+template <bool ALIGNED32>
+__global__ void __launch_bounds__(kChunkThreads, 1) crc_chunks_kernel(const uint8_t* __restrict__ data, uint64_t nchunks,
+                                                                      TreeOps ops, uint32_t* __restrict__ chunk_raw,
+                                                                      uint32_t zero) {
+  extern __shared__ __align__(16) uint32_t sm[];
+  uint32_t* slice = sm;                  // [4][256][32]
+  uint32_t* optab = sm + kSliceWords;    // [kLevels][4][256]
+  uint32_t* wraw = optab + kOpWords;     // [warps]
+  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+  // tables: the 1024 distinct entries once (table k = k extra zero bytes),
+  // staged in the first 4 KB of the op-table area, then replicated per bank
+  // (conflict-free stores: lane L writes bank L)
+  for (uint32_t i = t; i < 256u; i += kChunkThreads) {
+    uint32_t e = crc_table_entry(i);
+    optab[i] = e;
 #pragma unroll
     for (int k = 1; k < 4; ++k) {
       e = (e >> 8) ^ crc_table_entry(e & 0xFFu);
-      table[k][t] = e;
+      optab[k * 256 + i] = e;
     }
   }
-  const uint64_t base = uint64_t(blockIdx.x) * kChunk;  // full chunks only
-  const uint4* src = reinterpret_cast<const uint4*>(data + base);
-  const bool aligned16 = (reinterpret_cast<uintptr_t>(data) & 15u) == 0;
-  if (aligned16) {
-#pragma unroll 4
-    for (uint32_t i = t; i < kChunk / 16; i += kCrcThreads) {
-      const uint4 v = __ldg(src + i);
-      uint32_t* d = wbuf + (i >> 4) * kPieceWords + (i & 15u) * 4;  // 16 uint4 per piece
-      d[0] = v.x;
-      d[1] = v.y;
-      d[2] = v.z;
-      d[3] = v.w;
+  __syncthreads();
+  for (uint32_t i = warp; i < 4u * 256u; i += kChunkThreads / 32) slice[i * 32u + lane] = optab[i];
+  __syncthreads();
+  for (uint32_t i = t; i < kOpWords; i += kChunkThreads) optab[i] = op_tab_entry(ops.op[i >> 10], i & 1023u);
+  __syncthreads();
+  const uint32_t* tl = slice + lane;
+  const uint32_t wic = warp % kWarpsPerChunk, cip = warp / kWarpsPerChunk;
+  const uint64_t passes = (nchunks + kChunksPerPass - 1) / kChunksPerPass;
+  for (uint64_t pass = blockIdx.x; pass < passes; pass += gridDim.x) {
+    const uint64_t chunk = pass * kChunksPerPass + cip;
+    uint32_t c = 0;
+    if (chunk < nchunks) {
+      const uint8_t* piece = data + chunk * kChunk + (uint64_t(wic) * 32u + lane) * kPiece;
+      uint32_t w[kPiece / 4];
+#pragma unroll
+      for (int s = 0; s < int(kPiece / 32); ++s) {
+        uint32_t* r = w + 8 * s;
+        if constexpr (ALIGNED32) {
+          asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+              : "l"(piece + 32 * s));
+        } else {  // any alignment: bytes (records are 256 B aligned in practice)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint8_t* b = piece + 32 * s + 4 * k;
+            r[k] = uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+          }
+        }
+      }
+      // every load in flight before the first lookup: ptxas otherwise sinks each
+      // load to its first use (one 32-byte load in flight per lane); `zero` (a
+      // kernel argument, always 0) makes the first word depend on all of them
+      uint32_t dep = 0;
+#pragma unroll
+      for (int s = 1; s < int(kPiece / 32); ++s) dep |= w[8 * s];
+      c = w[0] ^ (dep & zero);
+      c = tl[(3 * 256 + (c & 0xFFu)) << 5] ^ tl[(2 * 256 + ((c >> 8) & 0xFFu)) << 5] ^
+          tl[(256 + ((c >> 16) & 0xFFu)) << 5] ^ tl[(c >> 24) << 5];
+#pragma unroll
+      for (int k = 1; k < int(kPiece / 4); ++k) {  // 4 bytes per step, little-endian byte order
+        c ^= w[k];
+        c = tl[(3 * 256 + (c & 0xFFu)) << 5] ^ tl[(2 * 256 + ((c >> 8) & 0xFFu)) << 5] ^
+            tl[(256 + ((c >> 16) & 0xFFu)) << 5] ^ tl[(c >> 24) << 5];
+      }
     }
-  } else {
-    uint8_t* b = reinterpret_cast<uint8_t*>(wbuf);
-    for (uint32_t i = t; i < kChunk; i += kCrcThreads) b[(i >> 8) * kPieceWords * 4 + (i & 255u)] = data[base + i];
-  }
-  __syncthreads();
-  uint32_t c = 0;
-  const uint32_t* p = wbuf + t * kPieceWords;
-#pragma unroll 8
-  for (uint32_t k = 0; k < kPiece / 4; ++k) {  // 4 bytes per step (little-endian byte order)
-    c ^= p[k];
-    c = table[3][c & 0xFFu] ^ table[2][(c >> 8) & 0xFFu] ^ table[1][(c >> 16) & 0xFFu] ^ table[0][c >> 24];
-  }
-  part[t] = c;
-  __syncthreads();
-  // tree fold: at level l, piece pairs of 256*2^l bytes: left' = S^len(right)(left) ^ right
-  for (int l = 0; l < kLevels; ++l) {
-    const uint32_t stride = 1u << l;
-    if ((t & ((stride << 1) - 1)) == 0) part[t] = mat_apply(ops.op[l], part[t]) ^ part[t + stride];
+    // level l pairs runs of 2^l pieces: left' = S^(128 * 2^l)(left) ^ right
+#pragma unroll
+    for (int l = 0; l < 5; ++l) {
+      const uint32_t o = __shfl_down_sync(0xFFFFFFFFu, c, 1u << l);
+      const uint32_t f = op_apply_tab(optab + l * 1024, c) ^ o;
+      if ((lane & ((2u << l) - 1u)) == 0) c = f;
+    }
+    if (lane == 0) wraw[warp] = c;
+    __syncthreads();
+    if (wic == 0) {  // the chunk's 16 warp raws, levels 5..8
+      uint32_t v = lane < uint32_t(kWarpsPerChunk) ? wraw[warp + lane] : 0u;
+#pragma unroll
+      for (int l = 5; l < kLevels; ++l) {
+        const uint32_t o = __shfl_down_sync(0xFFFFFFFFu, v, 1u << (l - 5));
+        const uint32_t f = op_apply_tab(optab + l * 1024, v) ^ o;
+        if ((lane & ((2u << (l - 5)) - 1u)) == 0) v = f;
+      }
+      if (lane == 0 && chunk < nchunks) chunk_raw[chunk] = v;
+    }
     __syncthreads();
   }
-  if (t == 0) chunk_raw[blockIdx.x] = part[0];
-  (void)n;
 }
 
-// one CTA: (1) thread t folds chunk CRCs [t*per, (t+1)*per) in order, (2) the
-// tail (< 64 KB) in 256-byte pieces in parallel, (3) thread 0 folds the range
-// CRCs and the tail pieces in order and applies the conditioning.  Every
-// operator is precomputed on the host (S^n for the record length included).
+// Level 2, one CTA, as trees (no serial chain):
+// (1) the chunk raws, front-padded with virtual zero chunks to 256 x per
+//     (raw(0^k || M) = raw(M): leading zeros are free): thread t loads its
+//     `per` consecutive raws, folds them with S^65536, then an 8-level tree
+//     with S^(per * 64 KB * 2^l);
+// (2) the tail (< 64 KB) as one front-padded virtual chunk: thread t's
+//     256-byte piece by table, then the 8-level S^(256 * 2^l) tree;
+// (3) raw = S^|tail|(chunks) ^ tail, crc = ~(S^n(~0) ^ raw).
+// Operators depend on n only: precomputed on the host, cached per n.
 struct FinalOps {
-  Mat chunk;       // S^65536
-  Mat range;       // S^(per * 65536)
-  Mat last_range;  // S^(len of the last range)
-  Mat piece;       // S^256
-  Mat tail_last;   // S^(len of the last tail piece)
-  Mat total;       // S^n
+  Mat unit;                  // S^65536
+  Mat range[kFinLevels];     // S^(per * 65536 * 2^l)
+  Mat tailtree[kFinLevels];  // S^(256 * 2^l)
+  Mat tail;                  // S^|tail|
+  Mat total;                 // S^n
 };
-__global__ void __launch_bounds__(kCrcThreads) crc_final_kernel(const uint8_t* __restrict__ data, uint64_t n,
+__global__ void __launch_bounds__(kFinThreads) crc_final_kernel(const uint8_t* __restrict__ data, uint64_t n,
                                                                 uint64_t nchunks, uint64_t per,
                                                                 const uint32_t* __restrict__ chunk_raw, FinalOps ops,
                                                                 uint32_t* out) {
   __shared__ uint32_t table[256];
-  __shared__ uint32_t part[kCrcThreads];
-  __shared__ uint32_t rng[kCrcThreads];
+  __shared__ uint32_t utab[1024];
+  __shared__ uint32_t rng[kFinThreads];
+  __shared__ uint32_t part[kFinThreads];
   const uint32_t t = threadIdx.x;
   table[t] = crc_table_entry(t);
+  for (uint32_t i = t; i < 1024u; i += kFinThreads) utab[i] = op_tab_entry(ops.unit, i);
+  __syncthreads();
   {
+    const uint64_t pad = uint64_t(kFinThreads) * per - nchunks;  // virtual zero chunks in front
     uint32_t r = 0;
-    const uint64_t c0 = uint64_t(t) * per, c1 = c0 + per < nchunks ? c0 + per : nchunks;
-    for (uint64_t i = c0; i < c1; ++i) r = mat_apply(ops.chunk, r) ^ chunk_raw[i];
+    constexpr int kBatch = 16;  // independent loads in flight, then the dependent fold
+    for (uint64_t v0 = uint64_t(t) * per; v0 < uint64_t(t + 1) * per; v0 += kBatch) {
+      uint32_t x[kBatch];
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) {
+        const uint64_t v = v0 + j;
+        x[j] = (v < uint64_t(t + 1) * per && v >= pad) ? chunk_raw[v - pad] : 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j)
+        if (v0 + j < uint64_t(t + 1) * per && v0 + j >= pad) r = op_apply_tab(utab, r) ^ x[j];
+    }
     rng[t] = r;
   }
-  __syncthreads();
   const uint64_t tail0 = nchunks * kChunk;
-  const uint64_t tail = n - tail0;  // < kChunk
-  const uint64_t b0 = tail0 + uint64_t(t) * kPiece;
-  uint32_t c = 0;
-  for (uint64_t i = b0; i < b0 + kPiece && i < n; ++i) c = table[(c ^ data[i]) & 0xFFu] ^ (c >> 8);
-  part[t] = c;
+  const uint32_t start = kChunk - static_cast<uint32_t>(n - tail0);  // first real byte of the virtual tail chunk
+  {
+    uint32_t c = 0;
+    const uint32_t b0 = t * kTailPiece;
+    for (uint32_t i = (b0 > start ? b0 : start); i < b0 + kTailPiece; ++i)
+      c = table[(c ^ data[tail0 + (i - start)]) & 0xFFu] ^ (c >> 8);
+    part[t] = c;
+  }
   __syncthreads();
-  if (t != 0) return;
-  uint32_t r = 0;
-  const uint64_t nranges = per ? (nchunks + per - 1) / per : 0;
-  for (uint64_t i = 0; i + 1 < nranges; ++i) r = mat_apply(ops.range, r) ^ rng[i];
-  if (nranges) r = mat_apply(ops.last_range, r) ^ rng[nranges - 1];
-  const uint32_t npieces = static_cast<uint32_t>((tail + kPiece - 1) / kPiece);
-  for (uint32_t i = 0; i + 1 < npieces; ++i) r = mat_apply(ops.piece, r) ^ part[i];
-  if (npieces) r = mat_apply(ops.tail_last, r) ^ part[npieces - 1];
-  *out = ~(mat_apply(ops.total, 0xFFFFFFFFu) ^ r);
+  for (int l = 0; l < kFinLevels; ++l) {  // both trees, level by level
+    const uint32_t stride = 1u << l;
+    if ((t & ((stride << 1) - 1)) == 0) {
+      rng[t] = mat_apply(ops.range[l], rng[t]) ^ rng[t + stride];
+      part[t] = mat_apply(ops.tailtree[l], part[t]) ^ part[t + stride];
+    }
+    __syncthreads();
+  }
+  if (t == 0) *out = ~(mat_apply(ops.total, 0xFFFFFFFFu) ^ mat_apply(ops.tail, rng[0]) ^ part[0]);
 }
 
 struct CrcOps {
   TreeOps tree;
-  Mat chunk;
   Mat pow2[48];  // S^(2^k bytes)
 };
 CrcOps make_crc_ops() {
   CrcOps ops;
   const Mat b = op_one_byte();
   for (int l = 0; l < kLevels; ++l) ops.tree.op[l] = op_pow(b, uint64_t(kPiece) << l);
-  ops.chunk = op_pow(b, kChunk);
   ops.pow2[0] = b;
   for (int k = 1; k < 48; ++k) ops.pow2[k] = mat_mul(ops.pow2[k - 1], ops.pow2[k - 1]);
   return ops;
@@ -212,26 +291,38 @@ Mat op_pow_fast(uint64_t n) {
 
 }  // namespace
 
-// scratch: >= max(1, n / 64 KB) uint32 device words
+// scratch: >= crc32_scratch_words(n) uint32 device words
 int launch_crc32(const void* data, uint64_t n, uint32_t* out_dev, uint32_t* scratch, void* stream) {
   auto st = static_cast<cudaStream_t>(stream);
   const CrcOps& ops = crc_ops();
   const uint64_t nchunks = n / kChunk;
   static DeviceOnce once;
-  const int se = once.run([](int) {
-    return static_cast<int>(cudaFuncSetAttribute(crc_chunks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(kChunkSmem)));
+  static int num_sms = 0;
+  const int se = once.run([](int dev) {
+    cudaError_t e = cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(crc_chunks_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kChunkSmem));
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(crc_chunks_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(kChunkSmem));
+    return static_cast<int>(e);
   });
   if (se) return se;
   if (nchunks) {
-    crc_chunks_kernel<<<static_cast<unsigned>(nchunks), kCrcThreads, kChunkSmem, st>>>(
-        static_cast<const uint8_t*>(data), n, ops.tree, scratch);
+    const uint64_t passes = (nchunks + kChunksPerPass - 1) / kChunksPerPass;
+    const unsigned grid = static_cast<unsigned>(passes < uint64_t(num_sms) ? passes : uint64_t(num_sms));
+    // 256-bit loads need 32-byte aligned pieces (records are cudaMalloc'd or
+    // pool-allocated, 256 B aligned); any other address takes the byte-load variant
+    auto* d8 = static_cast<const uint8_t*>(data);
+    if ((reinterpret_cast<uintptr_t>(data) & 31u) == 0)
+      crc_chunks_kernel<true><<<grid, kChunkThreads, kChunkSmem, st>>>(d8, nchunks, ops.tree, scratch, 0u);
+    else
+      crc_chunks_kernel<false><<<grid, kChunkThreads, kChunkSmem, st>>>(d8, nchunks, ops.tree, scratch, 0u);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  const uint64_t per = (nchunks + kCrcThreads - 1) / kCrcThreads;
-  const uint64_t nranges = per ? (nchunks + per - 1) / per : 0;
-  const uint64_t tail = n - nchunks * kChunk;
+  const uint64_t per = (nchunks + kFinThreads - 1) / kFinThreads;
   // the operators depend on n only: one cached set per length (records repeat their size)
   static std::mutex mu;
   static uint64_t cached_n = ~uint64_t(0);
@@ -240,18 +331,22 @@ int launch_crc32(const void* data, uint64_t n, uint32_t* out_dev, uint32_t* scra
   {
     std::lock_guard<std::mutex> lk(mu);
     if (cached_n != n) {
-      cached.chunk = ops.chunk;
-      cached.range = op_pow_fast(per * kChunk);
-      cached.last_range = nranges ? op_pow_fast((nchunks - (nranges - 1) * per) * kChunk) : mat_identity();
-      cached.piece = ops.tree.op[0];
-      cached.tail_last = tail ? op_pow_fast(tail - (tail - 1) / kPiece * kPiece) : mat_identity();
+      cached.unit = op_pow_fast(kChunk);
+      Mat r = op_pow_fast(per * kChunk), q = op_pow_fast(kTailPiece);
+      for (int l = 0; l < kFinLevels; ++l) {
+        cached.range[l] = r;
+        cached.tailtree[l] = q;
+        r = mat_mul(r, r);
+        q = mat_mul(q, q);
+      }
+      cached.tail = op_pow_fast(n - nchunks * kChunk);
       cached.total = op_pow_fast(n);
       cached_n = n;
     }
     fo = cached;
   }
-  crc_final_kernel<<<1, kCrcThreads, 0, st>>>(static_cast<const uint8_t*>(data), n, nchunks, per, scratch, fo,
-                                              out_dev);
+  crc_final_kernel<<<1, kFinThreads, 0, st>>>(static_cast<const uint8_t*>(data), n, nchunks, per, scratch, fo,
+                                               out_dev);
   return static_cast<int>(cudaGetLastError());
 }
 

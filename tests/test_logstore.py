@@ -68,6 +68,18 @@ def test_crc32_device_matches_reference(ref, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("offset", [1, 4, 16, 32])
+@pytest.mark.parametrize("n", [65536 * 5 + 7, 1_000_003])
+def test_crc32_device_any_alignment(ref, offset, n):
+    """The chunk kernel reads 32-byte aligned pieces with 256-bit loads and
+    takes a byte-load variant for any other address: same CRC either way."""
+    rng = np.random.default_rng(offset)
+    data = rng.integers(0, 256, n + offset, dtype=np.uint8).tobytes()
+    t = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()[offset:]
+    assert logstore.crc32_device(t) == ref.crc32(data[offset:])
+
+
+@pytest.mark.gpu
 def test_logger_roundtrip_and_replay_from_files(tmp_path):
     from paper_2302_06173_b200 import ADAM, OptimizerHyper
     from paper_2302_06173_b200.replay import BoundaryLog, Pipeline, Stage, replay_group
