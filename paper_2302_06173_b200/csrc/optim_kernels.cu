@@ -196,7 +196,22 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+#ifndef RW_OPTIM_WAIT_HINT_NS
+#define RW_OPTIM_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+#if RW_OPTIM_WAIT_HINT_NS
+  // suspend-time hint: waiting warps are parked until the tile lands
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(uint32_t(RW_OPTIM_WAIT_HINT_NS))
+      : "memory");
+#else
   asm volatile(
       "{\n"
       ".reg .pred P1;\n"
@@ -206,6 +221,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
   asm volatile(

@@ -74,10 +74,27 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 }
 // Waits on an mbarrier phase.  A pipeline bug must not hang the GPU: after
 // ~2^34 cycles (several seconds) the kernel traps instead.
+#ifndef RWB_WAIT_HINT_NS
+#define RWB_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
   const long long t0 = clock64();
   while (true) {
+#if RWB_WAIT_HINT_NS
+    // suspend-time hint: the waiting warp is parked until the phase flips (or
+    // the hint elapses) instead of re-polling -- fewer issue slots and less
+    // power spent by the producer / epilogue warps while the MMAs run
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity), "r"(uint32_t(RWB_WAIT_HINT_NS))
+        : "memory");
+#else
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
@@ -87,6 +104,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "=r"(done)
         : "r"(smem_u32(b)), "r"(parity)
         : "memory");
+#endif
     if (done) return;
     if (clock64() - t0 > (1ll << 34)) __trap();
   }
@@ -493,7 +511,10 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
   tm = first_m + in % gsz;
   tn = in / gsz;
 }
-constexpr int kGroupM = 16;
+#ifndef RWB_GROUP_M
+#define RWB_GROUP_M 16
+#endif
+constexpr int kGroupM = RWB_GROUP_M;
 
 template <int BN>
 struct Cfg {
