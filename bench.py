@@ -468,8 +468,10 @@ def measure_e2e_host(st, h, steps: int):
     return times[1:], h2d, d2h
 
 
-def pcie_probe(nbytes: int = 1 << 30) -> dict:
-    """Pinned-memory copy bandwidths on this box: the e2e roofline."""
+def pcie_probe(nbytes: int = 1 << 31, reps: int = 5) -> dict:
+    """Pinned-memory copy bandwidths on this box (the e2e roofline): each
+    direction alone, and both directions at once (per direction, timed with
+    events on its own stream); best of `reps`."""
     import torch
     hb = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
     hb2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
@@ -477,26 +479,29 @@ def pcie_probe(nbytes: int = 1 << 30) -> dict:
     db2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
-    def timed(fn):
-        best = 1e9
-        for _ in range(3):
+    def timed(pairs):
+        best = [1e30] * len(pairs)
+        for _ in range(reps):
             torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            fn()
+            evs = []
+            for stream, fn in pairs:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    a.record(stream)
+                    fn()
+                    b.record(stream)
+                evs.append((a, b))
             torch.cuda.synchronize()
-            best = min(best, time.perf_counter() - t0)
-        return best
-    th = timed(lambda: db.copy_(hb, non_blocking=True))
-    td = timed(lambda: hb.copy_(db, non_blocking=True))
-
-    def both():
-        with torch.cuda.stream(s1):
-            db.copy_(hb, non_blocking=True)
-        with torch.cuda.stream(s2):
-            hb2.copy_(db2, non_blocking=True)
-    tb = timed(both)
-    return dict(h2d_gbs=round(nbytes / th / 1e9, 1), d2h_gbs=round(nbytes / td / 1e9, 1),
-                bidir_gbs_each=round(nbytes / tb / 1e9, 1))
+            best = [min(x, a.elapsed_time(b)) for x, (a, b) in zip(best, evs)]
+        return [nbytes / (ms * 1e-3) / 1e9 for ms in best]
+    up = lambda: db.copy_(hb, non_blocking=True)     # noqa: E731
+    down = lambda: hb2.copy_(db2, non_blocking=True)  # noqa: E731
+    (h2d,) = timed([(s1, up)])
+    (d2h,) = timed([(s2, down)])
+    bh, bd = timed([(s1, up), (s2, down)])
+    return dict(h2d_gbs=round(h2d, 1), d2h_gbs=round(d2h, 1), bidir_h2d_gbs=round(bh, 1),
+                bidir_d2h_gbs=round(bd, 1), bidir_gbs_each=round(min(bh, bd), 1), bytes=nbytes,
+                how=f"pinned <-> device copies of {nbytes >> 20} MiB, CUDA events, best of {reps}")
 
 
 def config1_crash(reps: int = 40) -> dict:
@@ -1078,8 +1083,9 @@ def run_b200(args) -> None:
             e2e_ms = float(te.item())
             dist.barrier()
         pcie = pcie_probe()  # concurrently on every rank, like the e2e run
-        # roofline of the pipelined path: both directions concurrently at the bidirectional rate
-        e2e_roof_ms = max(h2d, d2h) / (pcie["bidir_gbs_each"] * 1e9) * 1e3
+        # roofline of the pipelined path: both directions concurrently, each at its
+        # measured bidirectional rate
+        e2e_roof_ms = max(h2d / (pcie["bidir_h2d_gbs"] * 1e9), d2h / (pcie["bidir_d2h_gbs"] * 1e9)) * 1e3
         e2e_val = nbytes * world / (e2e_ms * 1e-3) / 1e9
         del st
         torch.cuda.empty_cache()
@@ -1197,7 +1203,7 @@ def run_b200(args) -> None:
         "config2": other or None,
         "e2e": {"value": round(e2e_val, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms": round(e2e_ms, 3),
-                "pcie_bidir_gbs_each": pcie["bidir_gbs_each"], "roofline_ms": round(e2e_roof_ms, 2),
+                "pcie_bidir_gbs_each": pcie["bidir_gbs_each"], "pcie": pcie, "roofline_ms": round(e2e_roof_ms, 2),
                 "frac": round(e2e_roof_ms / e2e_ms, 3),
                 "path": "C-ABI rw_optimizer_undo_host, pinned host buffers, per-slice H2D|undo|D2H on 3 streams"},
         "gpu_launches": args.steps,  # one fused undo kernel per timed step

@@ -75,7 +75,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 // Waits on an mbarrier phase.  A pipeline bug must not hang the GPU: after
 // ~2^34 cycles (several seconds) the kernel traps instead.
 #ifndef RWB_WAIT_HINT_NS
-#define RWB_WAIT_HINT_NS 0
+#define RWB_WAIT_HINT_NS 200000
 #endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   uint32_t done = 0;
