@@ -27,7 +27,17 @@ namespace rwb {
 namespace gemm {
 
 constexpr int BM = 128;
-constexpr int BK = 64;     // 64 bf16 = 128 B = one swizzle atom row
+// K depth of one pipeline stage: 64 bf16 = 128 B rows (128-byte swizzle) or,
+// with RWB_GEMM_BK=32, 64 B rows (64-byte swizzle) and twice the stages in the
+// same shared memory -- a stage is released after 2 MMAs instead of 4, so the
+// loads in flight cover more of the memory latency.
+#ifndef RWB_GEMM_BK
+#define RWB_GEMM_BK 64
+#endif
+constexpr int BK = RWB_GEMM_BK;
+static_assert(BK == 64 || BK == 32, "BK: 64 (128B swizzle) or 32 (64B swizzle)");
+constexpr uint32_t kKRowBytes = BK * 2;                // K-major row = one swizzle atom row
+constexpr uint32_t kKSwizzleCode = BK == 64 ? 2u : 4u;  // SM100 descriptor layout: 128B / 64B swizzle
 constexpr int kThreads = 256;  // warp0 TMA, warp1 MMA, warp2 TMEM alloc, warps 4-7 epilogue
 constexpr int kEpiWarp0 = 4;
 
@@ -181,14 +191,20 @@ __device__ __forceinline__ void tmem_ld_32cols(uint32_t taddr, float* v) {
 //   K-major : rows of 128 B (64 bf16 of K); 8-row groups 1024 B apart (SBO).
 //   MN-major: rows of 128 B (64 bf16 of M/N) per K index; 8 K-rows = 1024 B
 //             (SBO); successive 64-wide M/N chunks LBO bytes apart.
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout = 2u /* SWIZZLE_128B */) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3FFFu);
   d |= uint64_t((lbo_bytes >> 4) & 0x3FFFu) << 16;
   d |= uint64_t((sbo_bytes >> 4) & 0x3FFFu) << 32;
   d |= uint64_t(1) << 46;  // version = 1 (Blackwell)
-  d |= uint64_t(2) << 61;  // layout = SWIZZLE_128B
+  d |= uint64_t(layout) << 61;
   return d;
+}
+// K-major operand, 16-element K step k inside the stage: +32 B along the row;
+// 8-row groups 8 x kKRowBytes apart (SBO)
+__device__ __forceinline__ uint64_t kmajor_desc(uint32_t base, int k) {
+  return make_desc(base + uint32_t(k) * 32u, 16, 8 * kKRowBytes, kKSwizzleCode);
 }
 
 // kind::f16 instruction descriptor: BF16 x BF16 -> F32, dense
@@ -521,7 +537,7 @@ struct Cfg {
 #ifdef RWB_GEMM_STAGES
   static constexpr int kStages = RWB_GEMM_STAGES;
 #else
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kStages = (BN == 256 ? 4 : 6) * (64 / BK);
 #endif
   static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB
   static constexpr uint32_t kBBytes = BN * BK * 2;   // 32 KB (BN=256)
@@ -532,7 +548,7 @@ struct Cfg {
 
 // smem layout inside one operand buffer for MN-major tiles: TMA boxes of
 // {64 (MN), 64 (K)} stacked along MN every 64*128 B = 8 KB  => LBO = 8192.
-constexpr uint32_t kMnChunkBytes = 64 * 128;
+constexpr uint32_t kMnChunkBytes = 64 * 2 * BK;  // one 64-wide MN chunk x BK K-rows of 128 B
 
 #ifdef RWB_PAIR_EXPERIMENT
 // tools/pair_probe.cu / tools/gemm_probe.cu instrumentation (per CTA):
@@ -676,9 +692,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per 16-element K step inside the 128 B swizzle row
             // MN-major: +2 K-row groups (2 x 1024 B) per 16-element K step
-            const uint64_t ad = AMAJ == K_MAJOR ? make_desc(sa + k * 32, 16, 1024)
+            const uint64_t ad = AMAJ == K_MAJOR ? kmajor_desc(sa, k)
                                                 : make_desc(sa + k * 2048, kMnChunkBytes, 1024);
-            const uint64_t bd = BMAJ == K_MAJOR ? make_desc(sb + k * 32, 16, 1024)
+            const uint64_t bd = BMAJ == K_MAJOR ? kmajor_desc(sb, k)
                                                 : make_desc(sb + k * 2048, kMnChunkBytes, 1024);
             tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
@@ -816,7 +832,7 @@ struct Cfg2 {
 #ifdef RWB_GEMM2_STAGES
   static constexpr int kStages = RWB_GEMM2_STAGES;
 #else
-  static constexpr int kStages = 6;
+  static constexpr int kStages = 6 * (64 / BK);
 #endif
   static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB: this CTA's 128 rows
   static constexpr uint32_t kBBytes = BNH * BK * 2;  // 16 KB: half of the B tile
@@ -967,9 +983,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t sb = sa + C::kABytes;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              const uint64_t ad = AMAJ == K_MAJOR ? make_desc(sa + k * 32, 16, 1024)
+              const uint64_t ad = AMAJ == K_MAJOR ? kmajor_desc(sa, k)
                                                   : make_desc(sa + k * 2048, kMnChunkBytes, 1024);
-              const uint64_t bd = BMAJ == K_MAJOR ? make_desc(sb + k * 32, 16, 1024)
+              const uint64_t bd = BMAJ == K_MAJOR ? kmajor_desc(sb, k)
                                                   : make_desc(sb + k * 2048, kMnChunkBytes, 1024);
               tc_mma2(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }

@@ -30,17 +30,19 @@ inline EncodeTiledFn encode_fn() {
 }
 
 // 2-D bf16 row-major matrix [rows, cols] (cols contiguous, row pitch ld
-// elements), box {64 cols, box_rows rows}, 128-byte swizzle, OOB -> zeros.
+// elements), box {box_cols cols, box_rows rows}, OOB -> zeros; the swizzle
+// follows the box row (128 B -> 128-byte swizzle, 64 B -> 64-byte swizzle).
 inline int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                    uint32_t box_rows) {
+                    uint32_t box_rows, uint32_t box_cols = 64) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return static_cast<int>(cudaErrorNotSupported);
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                                                       : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
 }
@@ -83,9 +85,10 @@ template <int BN, int AMAJ, int BMAJ, int EPI>
 int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
            cudaStream_t stream, int max_ctas = 0) {
   CUtensorMap ma, mb;
-  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM) : make_map(&ma, A, K, M, lda, 64);
+  // K-major: box {BK of K, rows}; MN-major: box {64 of M/N, BK K-rows}
+  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM, BK) : make_map(&ma, A, K, M, lda, BK);
   if (e) return e;
-  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN) : make_map(&mb, B, K, N, ldb, 64);
+  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN, BK) : make_map(&mb, B, K, N, ldb, BK);
   if (e) return e;
   EpiArgs epx = ep;
   CUtensorMap mo{}, mi{};
@@ -121,9 +124,9 @@ template <int BN, int AMAJ, int BMAJ, int EPI>
 int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
             cudaStream_t stream, int max_ctas = 0) {
   CUtensorMap ma, mb;
-  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM) : make_map(&ma, A, K, M, lda, 64);
+  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM, BK) : make_map(&ma, A, K, M, lda, BK);
   if (e) return e;
-  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN / 2) : make_map(&mb, B, K, N, ldb, 64);
+  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN / 2, BK) : make_map(&mb, B, K, N, ldb, BK);
   if (e) return e;
   EpiArgs epx = ep;
   CUtensorMap mo{}, mi{};

@@ -4,7 +4,7 @@ import sys
 import time
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.append(str(Path(__file__).resolve().parents[1]))  # a PYTHONPATH build variant wins
 
 import torch  # noqa: E402
 

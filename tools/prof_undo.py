@@ -4,7 +4,7 @@ so `ncu -k regex:optim_kernel -s 3 -c 1` captures an undo launch."""
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.append(str(Path(__file__).resolve().parents[1]))  # a PYTHONPATH build variant wins
 
 import torch  # noqa: E402
 

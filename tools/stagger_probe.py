@@ -6,7 +6,7 @@ import statistics
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.append(str(Path(__file__).resolve().parents[1]))  # a PYTHONPATH build variant wins
 import torch  # noqa: E402
 
 import bench  # noqa: E402

@@ -12,13 +12,13 @@ import sys
 import time
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.append(str(Path(__file__).resolve().parents[1]))  # a PYTHONPATH build variant wins
 
 import torch  # noqa: E402
 
-from bench import ClockSampler  # noqa: E402
-from paper_2302_06173_b200 import ADAM  # noqa: E402
+from paper_2302_06173_b200 import ADAM  # noqa: E402  (before bench, which puts the repo first on sys.path)
 from paper_2302_06173_b200.replay import Stage, synth_inputs  # noqa: E402
+from bench import ClockSampler  # noqa: E402
 
 secs = float(sys.argv[1]) if len(sys.argv) > 1 else 4.0
 R, D, H = 16384, 4096, 16384
