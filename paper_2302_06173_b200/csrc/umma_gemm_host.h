@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include "internal.h"  // DeviceOnce
 #include "umma_gemm.cuh"
 
 namespace rwb {
