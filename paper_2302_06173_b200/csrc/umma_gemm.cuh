@@ -61,6 +61,7 @@ struct EpiArgs {
   const __nv_bfloat16* y;  // [M, N] row-major, ld ldy (EPI_DTANH_BF16)
   int64_t ldy;
   int tma_epi;           // set by the launcher: output (and y / old output) tiles move by TMA
+  int mn3;               // set by the launcher: bit 0 / 1 = the MN-major A / B map is 3-D (one TMA per stage)
   float* colsum;         // dtanh epilogues, TMA path: per 32-row block column sums of the bf16
   int64_t ldc;           //   output, colsum[(row / 32) * ldc + col] (fused db partials)
 };
@@ -127,6 +128,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 3-D box {64 MN, BK K-rows, n chunks}: an MN-major tile's 64-wide chunks in
+// one instruction (chunk c lands c x 64 x BK x 2 bytes further in smem)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+#ifndef RWB_TMA3D
+#define RWB_TMA3D 0
+#endif  // 1: MN-major operands whose M/N is a multiple of 64 load through 3-D maps
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -637,6 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int k0 = kb * BK;
           if constexpr (AMAJ == K_MAJOR) {
             tma_load_2d(sa, &tma_a, &full_bar[stage], k0, m0);  // box {64 K, 128 M}
+          } else if (ep.mn3 & 1) {
+            tma_load_3d(sa, &tma_a, &full_bar[stage], 0, k0, m0 / 64);  // box {64 M, 64 K, 2 chunks}
           } else {
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c)                    // boxes {64 M, 64 K}
@@ -644,6 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if constexpr (BMAJ == K_MAJOR) {
             tma_load_2d(sb, &tma_b, &full_bar[stage], k0, n0);  // box {64 K, BN N}
+          } else if (ep.mn3 & 2) {
+            tma_load_3d(sb, &tma_b, &full_bar[stage], 0, k0, n0 / 64);  // box {64 N, 64 K, BN/64 chunks}
           } else {
 #pragma unroll
             for (int c = 0; c < BN / 64; ++c)

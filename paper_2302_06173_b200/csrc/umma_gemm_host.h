@@ -48,6 +48,24 @@ inline int make_map(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
 }
 
+// MN-major operand [K rows, MN cols] (MN contiguous, pitch ld) as a 3-D tensor
+// {64 MN, K, MN / 64 chunks} (strides: ld x 2 bytes per K row, 128 bytes per
+// chunk), box {64, box_k, chunks}: one TMA instruction per stage lays the
+// chunks out 64 x box_k x 2 bytes apart, exactly as `chunks` 2-D boxes would.
+inline int make_map_mn3(CUtensorMap* map, const void* base, uint64_t k_rows, uint64_t mn_cols, uint64_t ld,
+                        uint32_t box_k, uint32_t chunks) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return static_cast<int>(cudaErrorNotSupported);
+  cuuint64_t dims[3] = {64, k_rows, (mn_cols + 63) / 64};
+  cuuint64_t strides[2] = {ld * 2, 128};
+  cuuint32_t box[3] = {64, box_k, chunks};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(cudaErrorInvalidValue);
+}
+
 // Epilogue staging box map: [rows, cols] row-major, element size esize, box
 // {128 bytes of columns, 32 rows}, 128-byte swizzle.  Fails (non-zero) when
 // the matrix cannot be a TMA operand (base not 16-byte aligned, pitch not a
@@ -86,12 +104,21 @@ template <int BN, int AMAJ, int BMAJ, int EPI>
 int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
            cudaStream_t stream, int max_ctas = 0) {
   CUtensorMap ma, mb;
-  // K-major: box {BK of K, rows}; MN-major: box {64 of M/N, BK K-rows}
-  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM, BK) : make_map(&ma, A, K, M, lda, BK);
+  // K-major: box {BK of K, rows}; MN-major: box {64 of M/N, BK K-rows}, or the
+  // whole tile's chunks as one 3-D box (RWB_TMA3D, M/N a multiple of 64 so no
+  // chunk reads past the matrix)
+  const bool a3 = RWB_TMA3D && AMAJ == MN_MAJOR && M % 64 == 0;
+  const bool b3 = RWB_TMA3D && BMAJ == MN_MAJOR && N % 64 == 0;
+  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM, BK)
+          : a3            ? make_map_mn3(&ma, A, K, M, lda, BK, BM / 64)
+                          : make_map(&ma, A, K, M, lda, BK);
   if (e) return e;
-  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN, BK) : make_map(&mb, B, K, N, ldb, BK);
+  e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN, BK)
+      : b3            ? make_map_mn3(&mb, B, K, N, ldb, BK, BN / 64)
+                      : make_map(&mb, B, K, N, ldb, BK);
   if (e) return e;
   EpiArgs epx = ep;
+  epx.mn3 = (a3 ? 1 : 0) | (b3 ? 2 : 0);
   CUtensorMap mo{}, mi{};
   {
     constexpr int es = epi_f32(EPI) ? 4 : 2;
