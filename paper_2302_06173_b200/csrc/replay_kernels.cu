@@ -23,7 +23,7 @@ namespace {
 
 using bf16 = __nv_bfloat16;
 constexpr int kBN = 256;
-constexpr int kPairDefault = 0;
+constexpr int kPairDefault = 2;  // the wide CTA-pair kernel (profiles/r02/engines3.log)
 
 __device__ __forceinline__ bf16 dtanh1(bf16 g, bf16 y) {
   // dz = dL/dy * (1 - y^2)   (model.cpp:113-120)
@@ -173,25 +173,28 @@ static int gemm_cap() {
 // GEMM engine: the single-CTA kernel (cta_group::1, M128) or the CTA-pair
 // kernel (cta_group::2, M256: each SM stages half of the B tile, so L2->SM
 // traffic per FLOP drops by a third).  RW_GEMM_PAIR=0/1 overrides the default.
+// pair = 2: the wide CTA-pair kernel (256 rows per CTA, 512 per pair).
 static int g_pair_override = -1;
-static bool use_pair() {
-  if (g_pair_override >= 0) return g_pair_override != 0;
+static int pair_mode() {
+  if (g_pair_override >= 0) return g_pair_override;
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("RW_GEMM_PAIR");
-    v = (e && *e) ? (std::atoi(e) != 0) : kPairDefault;
+    v = (e && *e) ? std::atoi(e) : kPairDefault;
   }
-  return v != 0;
+  return v;
 }
 int replay_set_gemm_engine(int epilogue, int pair) {
   gemm::tma_epi_override() = epilogue < 0 ? -1 : (epilogue != 0);
-  g_pair_override = pair < 0 ? -1 : (pair != 0);
+  g_pair_override = pair < 0 ? -1 : pair;
   return 0;
 }
 template <int AM, int BMJ, int EPI>
 static int gemm_run(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
                     const gemm::EpiArgs& ep, cudaStream_t st) {
-  if (use_pair()) return gemm::launch2<kBN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, st, gemm_cap());
+  const int pm = pair_mode();
+  if (pm == 2) return gemm::launch2<kBN, AM, BMJ, EPI, 2>(A, lda, B, ldb, M, N, K, ep, st, gemm_cap());
+  if (pm == 1) return gemm::launch2<kBN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, st, gemm_cap());
   return gemm::launch<kBN, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, st, gemm_cap());
 }
 

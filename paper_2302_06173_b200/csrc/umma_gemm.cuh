@@ -545,6 +545,13 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 #define RWB_GROUP_M 16
 #endif
 constexpr int kGroupM = RWB_GROUP_M;
+// the pair kernels' raster group in M rows: 16 single-CTA tiles' worth for
+// MH = 1 (8 pair tiles of 256 rows); 4096 rows = 8 pair tiles of 512 for MH = 2
+// (profiles/r02/gemm_variants7_wide.log, replay ms: 1024 / 2048 / 4096 rows -> 633-634 / 627-630 / 623-626)
+template <int MH>
+constexpr int group_tiles2() {
+  return MH == 1 ? kGroupM / 2 : 8;
+}
 
 template <int BN>
 struct Cfg {
@@ -844,30 +851,40 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
 }
 
 
-template <int BN>
+// MH = 128-row halves per CTA.  MH = 1: the pair computes a 256 x BN tile
+// (16 KB of A + 16 KB of B per CTA and k-block, 6 stages, two TMEM
+// accumulators so the epilogue overlaps the next tile).  MH = 2: each CTA
+// owns 256 rows, the pair a 512 x BN tile -- two MMAs per 16-deep K step
+// share the B operand, so L2->SM bytes per FLOP drop by another quarter
+// (32 KB A + 16 KB B per CTA and k-block, 4 stages); the two 256-column
+// accumulators fill TMEM, so the epilogue no longer overlaps the MMAs.
+template <int BN, int MH = 1>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;
 #ifdef RWB_GEMM2_STAGES
   static constexpr int kStages = RWB_GEMM2_STAGES;
 #else
-  static constexpr int kStages = 6 * (64 / BK);
+  static constexpr int kStages = (MH == 1 ? 6 : 4) * (64 / BK);
 #endif
-  static constexpr uint32_t kABytes = BM * BK * 2;   // 16 KB: this CTA's 128 rows
-  static constexpr uint32_t kBBytes = BNH * BK * 2;  // 16 KB: half of the B tile
+  static constexpr uint32_t kHalfBytes = BM * BK * 2;      // 16 KB: 128 rows of A
+  static constexpr uint32_t kABytes = MH * kHalfBytes;     // this CTA's MH x 128 rows
+  static constexpr uint32_t kBBytes = BNH * BK * 2;        // 16 KB: half of the B tile
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
-  static constexpr uint32_t kTmemCols = 2 * BN;
+  static constexpr int kNAcc = MH == 1 ? 2 : 1;            // accumulator stages in TMEM
+  static constexpr uint32_t kTmemCols = kNAcc * MH * BN;   // 512 either way
   static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmem + 1024;
 };
 
-template <int BN, int AMAJ, int BMAJ, int EPI>
+template <int BN, int AMAJ, int BMAJ, int EPI, int MH = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     umma_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ CUtensorMap tma_i,
                       int M, int N, int K, EpiArgs ep) {
-  using C = Cfg2<BN>;
+  using C = Cfg2<BN, MH>;
   constexpr int S = C::kStages;
   constexpr int BNH = C::BNH;
-  constexpr int PM = 2 * BM;  // rows per CTA pair
+  constexpr int NACC = C::kNAcc;
+  constexpr int PM = 2 * MH * BM;  // rows per CTA pair
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2], epi_bar[8];
@@ -888,7 +905,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&full_bar[i], 1);  // the leader's expect_tx arrive (bytes of BOTH CTAs' loads)
       mbar_init(&empty_bar[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NACC; ++i) {
       mbar_init(&tfull_bar[i], 1);
       mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
     }
@@ -917,8 +934,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int tile = cid; tile < num_tiles; tile += ncl) {
         int tm, tn;
-      tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
-        const int m0 = tm * PM + int(rank) * BM;     // this CTA's A rows
+      tile_coords(tile, tiles_m, tiles_n, group_tiles2<MH>(), tm, tn);
+        const int m0 = tm * PM + int(rank) * MH * BM;  // this CTA's A rows
         const int nb0 = tn * BN + int(rank) * BNH;   // this CTA's half of B
         for (int kb = 0; kb < num_kb; ++kb) {
 #ifdef RWB_PAIR_EXPERIMENT
@@ -951,7 +968,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tma_load_2d_2sm(sa, &tma_a, lbar, k0, m0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tma_load_2d_2sm(sa + c * kMnChunkBytes, &tma_a, lbar, m0 + c * 64, k0);
+            for (int c = 0; c < MH * BM / 64; ++c)
+              tma_load_2d_2sm(sa + c * kMnChunkBytes, &tma_a, lbar, m0 + c * 64, k0);
           }
           if constexpr (BMAJ == K_MAJOR) {
             tma_load_2d_2sm(sb, &tma_b, lbar, k0, nb0);
@@ -969,7 +987,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA only) =====================
     if (leader) {
-      constexpr uint32_t idesc = make_idesc(PM, BN, AMAJ, BMAJ);
+      constexpr uint32_t idesc = make_idesc(2 * BM, BN, AMAJ, BMAJ);  // M = 256 per pair instruction
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -986,7 +1004,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) g_pair_dbg[blockIdx.x][1] += clock64() - a0;
 #endif
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * MH * BN);
         for (int kb = 0; kb < num_kb; ++kb) {
 #ifdef RWB_PAIR_EXPERIMENT
           const long long f0 = clock64();
@@ -1001,11 +1019,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t sb = sa + C::kABytes;
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k) {
-              const uint64_t ad = AMAJ == K_MAJOR ? kmajor_desc(sa, k)
-                                                  : make_desc(sa + k * 2048, kMnChunkBytes, 1024);
               const uint64_t bd = BMAJ == K_MAJOR ? kmajor_desc(sb, k)
                                                   : make_desc(sb + k * 2048, kMnChunkBytes, 1024);
-              tc_mma2(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+              for (int h = 0; h < MH; ++h) {  // the row halves share the B operand
+                const uint32_t sah = sa + uint32_t(h) * C::kHalfBytes;
+                const uint64_t ad = AMAJ == K_MAJOR ? kmajor_desc(sah, k)
+                                                    : make_desc(sah + k * 2048, kMnChunkBytes, 1024);
+                tc_mma2(d_tmem + uint32_t(h * BN), ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              }
             }
             tc_commit2_mc(&empty_bar[stage]);  // frees this stage in BOTH CTAs
           }
@@ -1017,7 +1039,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         if (lane == 0) tc_commit2_mc(&tfull_bar[acc]);
         __syncwarp();
-        if (++acc == 2) {
+        if (++acc == NACC) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -1037,31 +1059,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = cid; tile < num_tiles; tile += ncl) {
       int tm, tn;
-      tile_coords(tile, tiles_m, tiles_n, kGroupM / 2, tm, tn);
-      const int r0 = tm * PM + int(rank) * BM + ew * 32;
-      const int row = r0 + lane;
-      const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t(acc * BN);
-      if (ep.tma_epi) {
-        if constexpr (epi_input(EPI)) {
-          if (lane == 0) {
-            bulk_wait_read<0>();
-            epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], tn * BN, r0);
+      tile_coords(tile, tiles_m, tiles_n, group_tiles2<MH>(), tm, tn);
+#pragma unroll 1
+      for (int h = 0; h < MH; ++h) {  // this CTA's row halves, accumulator h
+        const int r0 = tm * PM + int(rank) * MH * BM + h * BM + ew * 32;
+        const int row = r0 + lane;
+        const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t((acc * MH + h) * BN);
+        if (ep.tma_epi) {
+          if constexpr (epi_input(EPI)) {
+            if (lane == 0) {
+              bulk_wait_read<0>();
+              epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], tn * BN, r0);
+            }
           }
+          if (h == 0) {
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+          }
+          epilogue_tile_tma<BN, EPI>(tbase, r0, tn * BN, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+        } else {
+          YChunk y0;
+          if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
+          if (h == 0) {
+            mbar_wait(&tfull_bar[acc], acc_phase);
+            tc_fence_after();
+          }
+          epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
         }
-        mbar_wait(&tfull_bar[acc], acc_phase);
-        tc_fence_after();
-        epilogue_tile_tma<BN, EPI>(tbase, r0, tn * BN, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
-      } else {
-        YChunk y0;
-        if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
-        mbar_wait(&tfull_bar[acc], acc_phase);
-        tc_fence_after();
-        epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;
       }

@@ -147,12 +147,13 @@ int launch(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N,
   return static_cast<int>(cudaGetLastError());
 }
 
-// CTA-pair (cta_group::2) variant: same contract, M tiles of 256 per pair.
-template <int BN, int AMAJ, int BMAJ, int EPI>
+// CTA-pair (cta_group::2) variant: same contract, M tiles of 256 (MH = 1) or
+// 512 (MH = 2: 256 rows per CTA) per pair.
+template <int BN, int AMAJ, int BMAJ, int EPI, int MH = 1>
 int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K, const EpiArgs& ep,
             cudaStream_t stream, int max_ctas = 0) {
   CUtensorMap ma, mb;
-  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, BM, BK) : make_map(&ma, A, K, M, lda, BK);
+  int e = AMAJ == K_MAJOR ? make_map(&ma, A, M, K, lda, MH * BM, BK) : make_map(&ma, A, K, M, lda, BK);
   if (e) return e;
   e = BMAJ == K_MAJOR ? make_map(&mb, B, N, K, ldb, BN / 2, BK) : make_map(&mb, B, K, N, ldb, BK);
   if (e) return e;
@@ -167,21 +168,21 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
     if (ep.colsum && (!ok || !uses_y(EPI) || (ep.ldc & 1) || (reinterpret_cast<uintptr_t>(ep.colsum) & 7)))
       return static_cast<int>(cudaErrorNotSupported);
   }
-  auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI>;
+  auto kern = umma_gemm2_kernel<BN, AMAJ, BMAJ, EPI, MH>;
   static DeviceOnce once;  // the attribute is per device
   const int se = once.run([&](int) {
     return static_cast<int>(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 static_cast<int>(Cfg2<BN>::kSmem)));
+                                                 static_cast<int>(Cfg2<BN, MH>::kSmem)));
   });
   if (se) return se;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN);
+  const int tiles = ((M + 2 * MH * BM - 1) / (2 * MH * BM)) * ((N + BN - 1) / BN);
   int pairs = sms / 2;
   if (tiles < pairs) pairs = tiles;
   if (max_ctas > 0 && pairs * 2 > max_ctas) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
-  kern<<<pairs * 2, kThreads, Cfg2<BN>::kSmem, stream>>>(ma, mb, mo, mi, M, N, K, epx);
+  kern<<<pairs * 2, kThreads, Cfg2<BN, MH>::kSmem, stream>>>(ma, mb, mo, mi, M, N, K, epx);
   return static_cast<int>(cudaGetLastError());
 }
 

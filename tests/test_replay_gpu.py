@@ -101,15 +101,16 @@ def test_backward_is_deterministic():
 
 @pytest.mark.parametrize("rows,din,dh,dout", [(512, 256, 512, 256), (200, 96, 264, 56)])
 def test_gemm_engines_agree_bitwise(rows, din, dh, dout):
-    """The four GEMM engines (TMA-staged or register epilogue x single-CTA or
-    CTA-pair kernel) give the same bits for forward, backward with a fused
-    stage boundary, and the accumulated fp32 weight gradients (second
-    micro-batch: EPI_F32_ACC); the ragged shape exercises clipped TMA boxes."""
+    """The six GEMM engines (TMA-staged or register epilogue x single-CTA,
+    CTA-pair or wide CTA-pair kernel) give the same bits for forward, backward
+    with a fused stage boundary, and the accumulated fp32 weight gradients
+    (second micro-batch: EPI_F32_ACC); the ragged shape exercises clipped TMA
+    boxes (and, for the wide pair's 512-row tiles, whole out-of-range halves)."""
     from paper_2302_06173_b200.replay import LIB
     from paper_2302_06173_b200._lib import check
     results = []
     try:
-        for epi, pair in ((1, 0), (0, 0), (1, 1), (0, 1)):
+        for epi, pair in ((1, 0), (0, 0), (1, 1), (0, 1), (1, 2), (0, 2)):
             check(LIB.rw_replay_set_gemm_engine(epi, pair))
             st = Stage(3, din, dh, dout, 2, 5, ADAM)
             prev = synth_inputs(5, 0, 9, rows, din)  # stands for the previous stage's output

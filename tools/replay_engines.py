@@ -14,7 +14,7 @@ from paper_2302_06173_b200.replay import LIB  # noqa: E402
 rounds = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 dev = torch.device("cuda", 0)
 for r in range(rounds):
-    for pair in (0, 1):
+    for pair in (0, 1, 2):
         assert LIB.rw_replay_set_gemm_engine(1, pair) == 0
         out = bench.replay_bench(1, 0, dev, iters=2)
         print(f"round {r} pair={pair} ms/iter {out['ms_per_iteration']} TFLOP/s {out['tflops_aggregate']}",
