@@ -861,10 +861,16 @@ __device__ __forceinline__ void tc_commit2_mc(uint64_t* bar) {
 template <int BN, int MH = 1>
 struct Cfg2 {
   static constexpr int BNH = BN / 2;
+  // MH = 2: eight epilogue warps, one group of four per row half, drain the
+  // two accumulators concurrently (the MMAs wait for both); their staging
+  // boxes take the smem of the fourth stage (3 stages measure as fast as 4)
+  static constexpr int kEpiWarps = 4 * MH;
+  static constexpr int kThreads = 128 + 32 * kEpiWarps;
+  static constexpr uint32_t kEpiSmemT = kEpiWarps * 2 * kEpiBoxBytes;
 #ifdef RWB_GEMM2_STAGES
   static constexpr int kStages = RWB_GEMM2_STAGES;
 #else
-  static constexpr int kStages = (MH == 1 ? 6 : 4) * (64 / BK);
+  static constexpr int kStages = (MH == 1 ? 6 : 3) * (64 / BK);
 #endif
   static constexpr uint32_t kHalfBytes = BM * BK * 2;      // 16 KB: 128 rows of A
   static constexpr uint32_t kABytes = MH * kHalfBytes;     // this CTA's MH x 128 rows
@@ -872,11 +878,11 @@ struct Cfg2 {
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr int kNAcc = MH == 1 ? 2 : 1;            // accumulator stages in TMEM
   static constexpr uint32_t kTmemCols = kNAcc * MH * BN;   // 512 either way
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmem + 1024;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmemT + 1024;
 };
 
 template <int BN, int AMAJ, int BMAJ, int EPI, int MH = 1>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThreads, 1)
     umma_gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                       const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ CUtensorMap tma_i,
                       int M, int N, int K, EpiArgs ep) {
@@ -887,7 +893,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   constexpr int PM = 2 * MH * BM;  // rows per CTA pair
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2], epi_bar[8];
+  __shared__ uint64_t full_bar[S], empty_bar[S], tfull_bar[2], tempty_bar[2], epi_bar[2 * C::kEpiWarps];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -907,9 +913,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < NACC; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 8);  // 4 epilogue warps x 2 CTAs (leader's copy is used)
+      mbar_init(&tempty_bar[i], 2 * C::kEpiWarps);  // every epilogue warp of both CTAs (leader's copy is used)
     }
-    for (int i = 0; i < 8; ++i) mbar_init(&epi_bar[i], 1);
+    for (int i = 0; i < 2 * C::kEpiWarps; ++i) mbar_init(&epi_bar[i], 1);
     if (ep.tma_epi) {
       prefetch_tmap(&tma_o);
       if (epi_input(EPI)) prefetch_tmap(&tma_i);
@@ -1049,11 +1055,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #endif
     }
   } else if (warp >= kEpiWarp0) {
-    // ===================== epilogue (both CTAs, own 128 rows) =====================
-    const int ew = warp - kEpiWarp0;
+    // ===================== epilogue (both CTAs, own rows) =====================
+    const int ewg = warp - kEpiWarp0;   // epilogue warp index
+    const int ew = ewg & 3;             // TMEM lane quarter (== warp % 4)
+    const int hw = ewg >> 2;            // MH = 2: the row half this warp drains
     const uint32_t tempty_leader = mapa_rank0(smem_u32(&tempty_bar[0]));
-    uint8_t* ebuf = smem + S * C::kStageBytes + ew * 2 * kEpiBoxBytes;
-    uint64_t* ebar = &epi_bar[ew * 2];
+    uint8_t* ebuf = smem + S * C::kStageBytes + ewg * 2 * kEpiBoxBytes;
+    uint64_t* ebar = &epi_bar[ewg * 2];
     uint32_t seq = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -1061,7 +1069,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       int tm, tn;
       tile_coords(tile, tiles_m, tiles_n, group_tiles2<MH>(), tm, tn);
 #pragma unroll 1
-      for (int h = 0; h < MH; ++h) {  // this CTA's row halves, accumulator h
+      for (int h = hw; h < hw + 1; ++h) {  // this warp's row half (accumulator h)
         const int r0 = tm * PM + int(rank) * MH * BM + h * BM + ew * 32;
         const int row = r0 + lane;
         const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t((acc * MH + h) * BN);
@@ -1072,18 +1080,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], tn * BN, r0);
             }
           }
-          if (h == 0) {
-            mbar_wait(&tfull_bar[acc], acc_phase);
-            tc_fence_after();
-          }
+          mbar_wait(&tfull_bar[acc], acc_phase);
+          tc_fence_after();
           epilogue_tile_tma<BN, EPI>(tbase, r0, tn * BN, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
         } else {
           YChunk y0;
           if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
-          if (h == 0) {
-            mbar_wait(&tfull_bar[acc], acc_phase);
-            tc_fence_after();
-          }
+          mbar_wait(&tfull_bar[acc], acc_phase);
+          tc_fence_after();
           epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
         }
       }

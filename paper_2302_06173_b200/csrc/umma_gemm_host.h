@@ -182,7 +182,7 @@ int launch2(const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N
   int pairs = sms / 2;
   if (tiles < pairs) pairs = tiles;
   if (max_ctas > 0 && pairs * 2 > max_ctas) pairs = max_ctas / 2 > 0 ? max_ctas / 2 : 1;
-  kern<<<pairs * 2, kThreads, Cfg2<BN, MH>::kSmem, stream>>>(ma, mb, mo, mi, M, N, K, epx);
+  kern<<<pairs * 2, Cfg2<BN, MH>::kThreads, Cfg2<BN, MH>::kSmem, stream>>>(ma, mb, mo, mi, M, N, K, epx);
   return static_cast<int>(cudaGetLastError());
 }
 
