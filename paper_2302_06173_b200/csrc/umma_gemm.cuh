@@ -864,13 +864,17 @@ struct Cfg2 {
   // MH = 2: eight epilogue warps, one group of four per row half, drain the
   // two accumulators concurrently (the MMAs wait for both); their staging
   // boxes take the smem of the fourth stage (3 stages measure as fast as 4)
-  static constexpr int kEpiWarps = 4 * MH;
+#ifndef RWB_GEMM2_CQ
+#define RWB_GEMM2_CQ 1
+#endif
+  static constexpr int kCQ = MH == 2 ? RWB_GEMM2_CQ : 1;  // column slices per half (warps per lane quarter)
+  static constexpr int kEpiWarps = 4 * MH * kCQ;
   static constexpr int kThreads = 128 + 32 * kEpiWarps;
   static constexpr uint32_t kEpiSmemT = kEpiWarps * 2 * kEpiBoxBytes;
 #ifdef RWB_GEMM2_STAGES
   static constexpr int kStages = RWB_GEMM2_STAGES;
 #else
-  static constexpr int kStages = (MH == 1 ? 6 : 3) * (64 / BK);
+  static constexpr int kStages = (MH == 1 ? 6 : (kCQ == 1 ? 3 : 2)) * (64 / BK);
 #endif
   static constexpr uint32_t kHalfBytes = BM * BK * 2;      // 16 KB: 128 rows of A
   static constexpr uint32_t kABytes = MH * kHalfBytes;     // this CTA's MH x 128 rows
@@ -1058,7 +1062,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
     // ===================== epilogue (both CTAs, own rows) =====================
     const int ewg = warp - kEpiWarp0;   // epilogue warp index
     const int ew = ewg & 3;             // TMEM lane quarter (== warp % 4)
-    const int hw = ewg >> 2;            // MH = 2: the row half this warp drains
+    const int hw = (ewg >> 2) % MH;     // MH = 2: the row half this warp drains
+    const int cq = (ewg >> 2) / MH;     // its column slice of the half (kCQ slices)
+    constexpr int BNQ = BN / C::kCQ;
     const uint32_t tempty_leader = mapa_rank0(smem_u32(&tempty_bar[0]));
     uint8_t* ebuf = smem + S * C::kStageBytes + ewg * 2 * kEpiBoxBytes;
     uint64_t* ebar = &epi_bar[ewg * 2];
@@ -1072,23 +1078,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
       for (int h = hw; h < hw + 1; ++h) {  // this warp's row half (accumulator h)
         const int r0 = tm * PM + int(rank) * MH * BM + h * BM + ew * 32;
         const int row = r0 + lane;
-        const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t((acc * MH + h) * BN);
+        const int c0 = tn * BN + cq * BNQ;
+        const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t((acc * MH + h) * BN + cq * BNQ);
         if (ep.tma_epi) {
           if constexpr (epi_input(EPI)) {
             if (lane == 0) {
               bulk_wait_read<0>();
-              epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], tn * BN, r0);
+              epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], c0, r0);
             }
           }
           mbar_wait(&tfull_bar[acc], acc_phase);
           tc_fence_after();
-          epilogue_tile_tma<BN, EPI>(tbase, r0, tn * BN, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+          epilogue_tile_tma<BNQ, EPI>(tbase, r0, c0, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
         } else {
           YChunk y0;
-          if constexpr (uses_y(EPI)) load_y_chunk(ep, row, tn * BN, M, N, y0);
+          if constexpr (uses_y(EPI)) load_y_chunk(ep, row, c0, M, N, y0);
           mbar_wait(&tfull_bar[acc], acc_phase);
           tc_fence_after();
-          epilogue_tile<BN, EPI>(tbase, row, tn * BN, M, N, ep, &y0);
+          epilogue_tile<BNQ, EPI>(tbase, row, c0, M, N, ep, &y0);
         }
       }
       tc_fence_before();
