@@ -971,7 +971,7 @@ def replay_bench(world: int, rank: int, device, iters: int = 2, rows: int = 1638
                 roofline_ms_per_iteration=round(flop_it / (sus * world * 1e12) * 1e3, 2),
                 frac_of_bf16_sustained_aggregate=round(tflops / (sus * world), 4),
                 frac_of_bf16_burst_aggregate=round(tflops / (_peaks()["bf16_burst"] * world), 4),
-                gemm="tcgen05 kind::f16 M128xN256xK16, TMA SW128, TMEM double-buffered accumulators")
+                gemm="tcgen05.mma.cta_group::2 kind::f16 M256xN256xK16 on CTA pairs, 512x256 tile per pair (two MMAs per K step sharing B), TMA SW128, 3 x 48 KB stages, 8 epilogue warps")
 
 
 def replay_subpipeline_bench(world: int, rank: int, device, iters: int = 2, rows: int = 16384, m: int = 8,
