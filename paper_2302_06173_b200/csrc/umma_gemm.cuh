@@ -405,7 +405,7 @@ __device__ __forceinline__ void epi_load_box(const CUtensorMap* mi, uint8_t* buf
 }
 
 template <int BN, int EPI>
-__device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0, int N, const EpiArgs& ep,
+__device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0, int M, int N, const EpiArgs& ep,
                                                   const CUtensorMap* mo, const CUtensorMap* mi, uint8_t* ebuf,
                                                   uint64_t* ebar, uint32_t& seq) {
   constexpr int COLS = epi_f32(EPI) ? 32 : 64;
@@ -502,7 +502,9 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
     fence_proxy_async_smem();
     __syncwarp();
     if constexpr (uses_y(EPI)) {
-      if (ep.colsum) {  // db partials: lane l sums columns 2l, 2l+1 of the box over its 32 rows, in row order
+      // (a box wholly below the matrix -- the tail of a 256 / 512-row tile -- has no
+      // partial row to write: the buffer holds ceil(M / 32) of them)
+      if (ep.colsum && r0 < M) {  // db partials: lane l sums columns 2l, 2l+1 of the box over its 32 rows, in row order
         float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
         for (uint32_t r = 0; r < 32; ++r) {
@@ -770,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
-        epilogue_tile_tma<BN, EPI>(tbase, m0 + ew * 32, n0, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+        epilogue_tile_tma<BN, EPI>(tbase, m0 + ew * 32, n0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
       } else {
         YChunk y0;
         if constexpr (uses_y(EPI)) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
@@ -1089,7 +1091,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
           }
           mbar_wait(&tfull_bar[acc], acc_phase);
           tc_fence_after();
-          epilogue_tile_tma<BNQ, EPI>(tbase, r0, c0, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+          epilogue_tile_tma<BNQ, EPI>(tbase, r0, c0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
         } else {
           YChunk y0;
           if constexpr (uses_y(EPI)) load_y_chunk(ep, row, c0, M, N, y0);

@@ -163,6 +163,36 @@ def test_fused_db_matches_separate_column_sums(rows):
         assert (db_f[l] - db_u[l]).abs().max().item() <= 1e-5 * scale + 1e-7
 
 
+@pytest.mark.parametrize("pair", [0, 1, 2])
+def test_fused_db_partials_stay_inside_scratch(pair):
+    """The per-32-row db partials are written for rows < M only: the tail
+    boxes of a tile that hangs below the matrix (rows = 2100: the last 128-,
+    256- or 512-row tile is mostly out of range) must not write past the
+    ceil(rows / 32) partial rows the scratch holds."""
+    from paper_2302_06173_b200.replay import LIB
+    from paper_2302_06173_b200._lib import check
+    rows = 2100
+    check(LIB.rw_replay_set_gemm_engine(1, pair))
+    try:
+        st = Stage(2, 128, 512, 256, 3, 9, ADAM)
+        mx = max(st.dims)
+        need = (rows + 31) // 32 * mx
+        big = torch.full((need + 64 * mx,), float("nan"), dtype=torch.float32, device="cuda")
+        s0 = torch.empty(rows * mx, dtype=torch.bfloat16, device="cuda")
+        s1 = torch.empty(rows * mx, dtype=torch.bfloat16, device="cuda")
+        st._scratch[rows] = (s0, s1, big[:need])
+        prev = synth_inputs(9, 0, 7, rows, 128)
+        acts = st.new_acts(rows, synth_inputs(9, 0, 0, rows, 128))
+        st.forward(acts)
+        gout = torch.empty(rows, 128, dtype=torch.bfloat16, device="cuda")
+        st.backward(acts, synth_inputs(9, 1, 0, rows, 256), gout, accumulate=False, prev_y=prev, fuse_db=True)
+        torch.cuda.synchronize()
+        assert torch.isnan(big[need:]).all(), "db partials written past the scratch"
+        assert torch.isfinite(st.grad).all()
+    finally:
+        check(LIB.rw_replay_set_gemm_engine(-1, -1))
+
+
 def _pipeline(kind=ADAM):
     h = OptimizerHyper(kind=kind, lr=1e-3 if kind == ADAM else 0.05, weight_decay=0.01)
     return Pipeline(p=3, dim=64, hidden=128, layers=2, rows=128, micro_batches=4, seed=11, kind=kind,
