@@ -1104,10 +1104,24 @@ def run_b200(args) -> None:
             torch.cuda.empty_cache()
             m64 = statistics.median(t64)
             extras["adam340m_undo_f64"] = dict(ms=round(m64, 4), gbs=round(_gbs(nb64, m64), 1))
-            tsg, nbsg, ssg, _ = measure_undo(CONFIGS["sgdm10m"]["sizes"](), "sgdm", 20, 3)
-            del ssg
+            tsg, nbsg, ssg, hsg = measure_undo(CONFIGS["sgdm10m"]["sizes"](), "sgdm", 20, 3)
             msg = statistics.median(tsg)
-            extras["sgdm10m_undo_all"] = dict(ms=round(msg, 4), gbs=round(_gbs(nbsg, msg), 1))
+            # the kernel alone (CUPTI activity records): the event-bracketed time of a
+            # 40 us call also holds the launch gap behind the preceding step
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                for _ in range(10):
+                    ssg.step(hsg)
+                    ssg.undo(hsg)
+                torch.cuda.synchronize()
+            kus = [(e.time_range.end - e.time_range.start) for e in prof.events()
+                   if e.device_type.name == "CUDA" and "optim_kernel" in e.name
+                   and e.name.split("<", 1)[1].split(",")[2].strip() == "true"]
+            del ssg
+            kmed = statistics.median(kus) if kus else None
+            extras["sgdm10m_undo_all"] = dict(ms=round(msg, 4), gbs=round(_gbs(nbsg, msg), 1),
+                                              kernel_us=round(kmed, 1) if kmed else None,
+                                              kernel_gbs=round(nbsg / (kmed * 1e-6) / 1e9, 1) if kmed else None)
             extras["config1_crash"] = config1_crash()
             # the other kinds of Table 1 on the same 336M BERT-large layout
             by_kind = {}

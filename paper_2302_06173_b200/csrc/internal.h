@@ -41,7 +41,10 @@ struct Uniform {
 // Small calls carry their work list and scalar sets in the kernel's
 // parameter space (__grid_constant__) instead of a pinned H2D copy: no copy
 // on the stream ahead of the kernel, so a 50-group undo costs one launch.
-constexpr uint32_t kInlineItems = 128;
+#ifndef RW_INLINE_ITEMS
+#define RW_INLINE_ITEMS 128
+#endif
+constexpr uint32_t kInlineItems = RW_INLINE_ITEMS;
 constexpr uint32_t kInlineSets = 16;
 struct InlineMeta {
   WorkItem work[kInlineItems];
