@@ -442,8 +442,10 @@ int rw_replay_set_sm_reserve(int32_t n);
 /* Replay GEMM engine (process-wide; -1 keeps the default / environment):
  *   epilogue: 1 = output tiles staged in shared memory and written by TMA
  *             tensor stores (default), 0 = per-thread register stores;
- *   pair:     1 = CTA-pair kernel (tcgen05 cta_group::2, M = 256),
- *             0 = single-CTA kernel (default).
+ *   pair:     2 = wide CTA-pair kernel (cta_group::2, 256 rows per CTA,
+ *                 512 x 256 tiles per cluster; default),
+ *             1 = CTA-pair kernel (cta_group::2, 128 rows per CTA),
+ *             0 = single-CTA kernel (cta_group::1, M = 128).
  * Every combination gives the same bits (same MMA order, same epilogue
  * arithmetic); the knob exists for A/B measurements and tests. */
 int rw_replay_set_gemm_engine(int32_t epilogue, int32_t pair);
