@@ -353,7 +353,12 @@ int rw_apply_resolution(rw_state* s, const rw_hyper* h, const uint8_t* actions, 
  * m, v (and g with RW_RECOVER_INCLUDE_GRAD) to every other rank; markers and
  * LAMB trust stacks follow.  Every rank passes its own state of the same
  * layout; non-roots pass actions = NULL.  *bytes_out = bytes per replacement. */
-enum { RW_RECOVER_INCLUDE_GRAD = 1 };
+/* RW_RECOVER_CHAIN: instead of NCCL broadcasts, the resolved runs travel over
+ * the copy engines as a chain (root -> next rank -> ...): each rank maps its
+ * successor's buffers through CUDA IPC and forwards every run as soon as its
+ * epoch counter lands (one GPU per rank on one node; the fastest transfer for
+ * one replacement, profiles/r02). */
+enum { RW_RECOVER_INCLUDE_GRAD = 1, RW_RECOVER_CHAIN = 2 };
 int rw_recover_replication(rw_state* s, const rw_hyper* h, rw_comm* c, int32_t root, const uint8_t* actions,
                            int32_t strategy, uint32_t flags, uint32_t pieces, void* stream, uint64_t* bytes_out);
 

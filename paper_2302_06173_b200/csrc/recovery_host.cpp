@@ -20,10 +20,12 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -85,6 +87,13 @@ struct rw_comm {
   uint64_t* h_buf = nullptr;
   uint64_t* d_buf = nullptr;
   size_t buf_words = 0;
+  // copy-engine chain (RW_RECOVER_CHAIN): peers' allocations mapped through
+  // CUDA IPC once and kept (keyed by handle), the epoch counters the
+  // predecessor writes, and the epoch of the current call
+  std::vector<std::pair<std::array<uint8_t, 64>, void*>> ipc_maps;
+  uint64_t* chain_ctr = nullptr;
+  size_t chain_ctr_n = 0;
+  uint64_t chain_epoch = 0;
 };
 
 namespace {
@@ -197,6 +206,14 @@ int ensure_bufs(rw_comm* c, size_t words) {
   return RW_OK;
 }
 
+void free_chain(rw_comm* c) {
+  for (auto& m : c->ipc_maps) rw_ipc_close(m.second);
+  c->ipc_maps.clear();
+  if (c->chain_ctr) cudaFree(c->chain_ctr);
+  c->chain_ctr = nullptr;
+  c->chain_ctr_n = 0;
+}
+
 void free_bufs(rw_comm* c) {
   if (c->h_buf) cudaFreeHost(c->h_buf);
   if (c->d_buf) cudaFree(c->d_buf);
@@ -206,6 +223,166 @@ void free_bufs(rw_comm* c) {
 }
 
 }  // namespace
+
+// markers (and LAMB trust stacks) travel with the state: one broadcast from
+// the root once its undo has finished, written into every other rank's state
+static int replicate_meta(rw_comm* c, rw_state* s, const rw_hyper* h, int32_t root, std::vector<rw_group>& mk,
+                          void* stream) {
+  const uint32_t G = static_cast<uint32_t>(mk.size());
+  const bool is_root = c->rank == root;
+  auto cs = static_cast<cudaStream_t>(stream);
+  int st = RW_OK;
+  const int depth = RW_LAMB_TRUST_DEPTH;
+  const bool lamb = h->kind == RW_LAMB;
+  const size_t words = size_t(G) * 2 + (lamb ? size_t(G) * (depth + 1) : 0);
+  std::vector<uint64_t> meta(words ? words : 1);
+  if (is_root) {
+    HCUDA(cudaStreamSynchronize(cs));  // the undo's markers are final
+    if (G && (st = rw_state_read_groups(s, mk.data(), stream))) return st;
+    for (uint32_t i = 0; i < G; ++i) meta[2 * i] = mk[i].t, meta[2 * i + 1] = mk[i].updated;
+    if (lamb)
+      for (uint32_t i = 0; i < G; ++i) {
+        double vals[RW_LAMB_TRUST_DEPTH];
+        uint32_t cnt = 0;
+        if ((st = rw_state_saved_scalars(s, i, vals, depth, &cnt, stream))) return st;
+        uint64_t* row = meta.data() + 2 * G + size_t(i) * (depth + 1);
+        row[0] = cnt;
+        std::memcpy(row + 1, vals, sizeof(double) * cnt);
+      }
+  }
+  if (words) {
+    if ((st = ensure_bufs(c, words))) return st;
+    std::memcpy(c->h_buf, meta.data(), words * 8);
+    HCUDA(cudaMemcpyAsync(c->d_buf, c->h_buf, words * 8, cudaMemcpyHostToDevice, c->stream));
+    HNCCL(c, ncclBroadcast(c->d_buf, c->d_buf, words, ncclUint64, root, c->comm, c->stream));
+    if ((st = track(c))) return st;
+    HCUDA(cudaMemcpyAsync(c->h_buf, c->d_buf, words * 8, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if ((st = sync_comm(c, "recover_replication"))) return st;
+  if (words) std::memcpy(meta.data(), c->h_buf, words * 8);
+  if (!is_root) {
+    for (uint32_t i = 0; i < G; ++i) mk[i].t = meta[2 * i], mk[i].updated = static_cast<uint32_t>(meta[2 * i + 1]);
+    if (G && (st = rw_state_write_groups(s, mk.data(), stream))) return st;
+    if (lamb)
+      for (uint32_t i = 0; i < G; ++i) {
+        const uint64_t* row = meta.data() + 2 * G + size_t(i) * (depth + 1);
+        double vals[RW_LAMB_TRUST_DEPTH];
+        std::memcpy(vals, row + 1, sizeof(vals));
+        if ((st = rw_state_set_saved_scalars(s, i, vals, static_cast<uint32_t>(row[0]), stream))) return st;
+      }
+  }
+  return RW_OK;
+}
+
+// apply_undo + recover_replication over the copy engines, as a chain
+// (recovery.recover_replication_chain): ranks in the order root, then the
+// others ascending; every rank but the last maps its successor's buffers and
+// epoch counters through CUDA IPC (handles exchanged with one ncclAllGather);
+// the root undoes run i on the caller's stream while the communicator stream
+// copies run i-1 into the successor's HBM (cudaMemcpyAsync over NVLink, no
+// kernel) and bumps the successor's counter for that run; every other rank's
+// communicator stream waits for its own counter and forwards the run.
+static int chain_transfer(rw_comm* c, rw_state* s, const rw_hyper* h, int32_t root, const uint8_t* actions,
+                          bool undo, const std::vector<rw_group>& mk, uint64_t total, size_t es,
+                          const std::vector<void*>& bufs, const std::vector<std::pair<uint32_t, uint32_t>>& runs,
+                          cudaStream_t cs, uint64_t* bytes_out) {
+  const int n = c->size, nb = static_cast<int>(bufs.size());
+  const uint32_t G = static_cast<uint32_t>(mk.size());
+  const size_t npieces = runs.size();
+  if (c->chain_ctr_n < npieces) {  // counters persist across calls; epochs only grow
+    if (c->chain_ctr) cudaFree(c->chain_ctr);
+    HCUDA(cudaMalloc(&c->chain_ctr, std::max<size_t>(npieces, 16) * 8));
+    HCUDA(cudaMemset(c->chain_ctr, 0, std::max<size_t>(npieces, 16) * 8));
+    c->chain_ctr_n = std::max<size_t>(npieces, 16);
+    c->chain_epoch = 0;
+  }
+  uint64_t* counters = c->chain_ctr;
+  // every rank reallocates together (same npieces), so the epochs stay in step
+  const uint64_t epoch = ++c->chain_epoch;
+  // exchange: per rank nb + 1 records of (64-byte handle, 8-byte offset) = 9 words each
+  const size_t rec = 9, per = (nb + 1) * rec;
+  int st = ensure_bufs(c, per * n);
+  if (st) return st;
+  std::vector<uint64_t> mine(per, 0);
+  for (int b = 0; b <= nb; ++b) {
+    void* p = b < nb ? bufs[b] : static_cast<void*>(counters);
+    if ((st = rw_ipc_export(p, mine.data() + b * rec, &mine[b * rec + 8]))) return st;
+  }
+  std::memcpy(c->h_buf, mine.data(), per * 8);
+  HCUDA(cudaMemcpyAsync(c->d_buf + per * c->rank, c->h_buf, per * 8, cudaMemcpyHostToDevice, c->stream));
+  HNCCL(c, ncclAllGather(c->d_buf + per * c->rank, c->d_buf, per, ncclUint64, c->comm, c->stream));
+  if ((st = track(c))) return st;
+  HCUDA(cudaMemcpyAsync(c->h_buf, c->d_buf, per * n * 8, cudaMemcpyDeviceToHost, c->stream));
+  if ((st = sync_comm(c, "recover_replication (chain handles)"))) return st;
+  std::vector<int> chain{root};
+  for (int r = 0; r < n; ++r)
+    if (r != root) chain.push_back(r);
+  const int pos = static_cast<int>(std::find(chain.begin(), chain.end(), c->rank) - chain.begin());
+  const int next = pos + 1 < n ? chain[pos + 1] : -1;
+  std::vector<char*> dst(nb + 1, nullptr);
+  if (next >= 0) {
+    const uint64_t* rec0 = c->h_buf + per * next;
+    for (int b = 0; b <= nb; ++b) {
+      std::array<uint8_t, 64> key;
+      std::memcpy(key.data(), rec0 + b * rec, 64);
+      void* base = nullptr;
+      for (auto& m : c->ipc_maps)
+        if (m.first == key) base = m.second;
+      if (!base) {  // map each allocation of the successor once per communicator
+        if ((st = rw_ipc_import(key.data(), &base))) return st;
+        c->ipc_maps.emplace_back(key, base);
+      }
+      dst[b] = static_cast<char*>(base) + rec0[b * rec + 8];
+    }
+  }
+  cudaEvent_t ev;
+  HCUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  constexpr size_t kLead = 2;
+  std::vector<cudaEvent_t> copied(npieces, nullptr);
+  for (auto& e : copied) HCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  uint64_t bytes = 0;
+  for (size_t k = 0; k < npieces; ++k) {
+    const uint32_t g0 = runs[k].first, g1 = runs[k].second;
+    const uint64_t lo = g0 == 0 ? 0 : mk[g0].offset, hi = g1 < G ? mk[g1].offset : total;
+    if (pos == 0) {
+      if (undo) {
+        std::vector<uint32_t> ids;
+        for (uint32_t i = g0; i < g1; ++i)
+          if (actions[i] == RW_ACT_UNDO) ids.push_back(i);
+        // pace the undo two runs ahead of the copies: a burst of every run's
+        // undo at full HBM bandwidth would starve the copy engines' reads
+        if (!ids.empty() && k >= kLead) HCUDA(cudaStreamWaitEvent(cs, copied[k - kLead], 0));
+        if (!ids.empty() && (st = rw_optimizer_undo(s, h, ids.data(), static_cast<uint32_t>(ids.size()), cs)))
+          return st;
+      }
+      HCUDA(cudaEventRecord(ev, cs));
+      HCUDA(cudaStreamWaitEvent(c->stream, ev, 0));
+    } else if ((st = rw_stream_wait_u64(c->stream, counters + k, epoch))) {  // the predecessor's copy landed
+      return st;
+    }
+    if (next >= 0) {
+      std::vector<void*> d(nb);
+      std::vector<const void*> src(nb);
+      std::vector<uint64_t> len(nb, (hi - lo) * es);
+      for (int b = 0; b < nb; ++b) {
+        d[b] = dst[b] + lo * es;
+        src[b] = static_cast<const char*>(bufs[b]) + lo * es;
+      }
+      if ((st = rw_copy_async(d.data(), src.data(), len.data(), static_cast<uint32_t>(nb), c->stream))) return st;
+      if ((st = rw_stream_write_u64(c->stream, reinterpret_cast<uint64_t*>(dst[nb]) + k, epoch))) return st;
+      if (pos == 0) HCUDA(cudaEventRecord(copied[k], c->stream));
+    }
+    bytes += (hi - lo) * es * nb;
+  }
+  cudaEventDestroy(ev);
+  for (auto& e : copied) cudaEventDestroy(e);
+  // every hop has landed everywhere before anyone moves on (the next call may
+  // overwrite the same buffers)
+  HNCCL(c, ncclAllReduce(c->d_buf, c->d_buf, 1, ncclUint64, ncclMax, c->comm, c->stream));
+  if ((st = track(c))) return st;
+  *bytes_out = bytes;
+  return RW_OK;
+}
 
 extern "C" {
 
@@ -286,6 +463,7 @@ int rw_comm_destroy(rw_comm* c) {
     }
   }
   if (c->stream) cudaStreamDestroy(c->stream);
+  free_chain(c);
   free_bufs(c);
   delete c;
   return st;
@@ -298,6 +476,7 @@ int rw_comm_abort(rw_comm* c) {
   if (c->comm) ncclCommAbort(c->comm);
   c->comm = nullptr;
   if (c->stream) cudaStreamDestroy(c->stream);
+  free_chain(c);
   free_bufs(c);
   delete c;
   return RW_OK;
@@ -636,6 +815,14 @@ int rw_recover_replication(rw_state* s, const rw_hyper* h, rw_comm* c, int32_t r
   }
   auto cs = static_cast<cudaStream_t>(stream);
   if ((st = order_after(c->stream, cs))) return st;
+  if (flags & RW_RECOVER_CHAIN) {
+    uint64_t bytes = 0;
+    if ((st = chain_transfer(c, s, h, root, actions, undo, mk, total, es, bufs, runs, cs, &bytes))) return st;
+    if ((st = replicate_meta(c, s, h, root, mk, stream))) return st;
+    if ((st = order_after(cs, c->stream))) return st;
+    if (bytes_out) *bytes_out = bytes;
+    return RW_OK;
+  }
   cudaEvent_t ev;
   HCUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   uint64_t bytes = 0;
@@ -662,46 +849,7 @@ int rw_recover_replication(rw_state* s, const rw_hyper* h, rw_comm* c, int32_t r
     bytes += (hi - lo) * es * bufs.size();
   }
   cudaEventDestroy(ev);
-  // markers (and LAMB trust stacks) travel with the state
-  const int depth = RW_LAMB_TRUST_DEPTH;
-  const bool lamb = h->kind == RW_LAMB;
-  const size_t words = size_t(G) * 2 + (lamb ? size_t(G) * (depth + 1) : 0);
-  std::vector<uint64_t> meta(words ? words : 1);
-  if (is_root) {
-    HCUDA(cudaStreamSynchronize(cs));  // the undo's markers are final
-    if (G && (st = rw_state_read_groups(s, mk.data(), stream))) return st;
-    for (uint32_t i = 0; i < G; ++i) meta[2 * i] = mk[i].t, meta[2 * i + 1] = mk[i].updated;
-    if (lamb)
-      for (uint32_t i = 0; i < G; ++i) {
-        double vals[RW_LAMB_TRUST_DEPTH];
-        uint32_t cnt = 0;
-        if ((st = rw_state_saved_scalars(s, i, vals, depth, &cnt, stream))) return st;
-        uint64_t* row = meta.data() + 2 * G + size_t(i) * (depth + 1);
-        row[0] = cnt;
-        std::memcpy(row + 1, vals, sizeof(double) * cnt);
-      }
-  }
-  if (words) {
-    if ((st = ensure_bufs(c, words))) return st;
-    std::memcpy(c->h_buf, meta.data(), words * 8);
-    HCUDA(cudaMemcpyAsync(c->d_buf, c->h_buf, words * 8, cudaMemcpyHostToDevice, c->stream));
-    HNCCL(c, ncclBroadcast(c->d_buf, c->d_buf, words, ncclUint64, root, c->comm, c->stream));
-    if ((st = track(c))) return st;
-    HCUDA(cudaMemcpyAsync(c->h_buf, c->d_buf, words * 8, cudaMemcpyDeviceToHost, c->stream));
-  }
-  if ((st = sync_comm(c, "recover_replication"))) return st;
-  if (words) std::memcpy(meta.data(), c->h_buf, words * 8);
-  if (!is_root) {
-    for (uint32_t i = 0; i < G; ++i) mk[i].t = meta[2 * i], mk[i].updated = static_cast<uint32_t>(meta[2 * i + 1]);
-    if (G && (st = rw_state_write_groups(s, mk.data(), stream))) return st;
-    if (lamb)
-      for (uint32_t i = 0; i < G; ++i) {
-        const uint64_t* row = meta.data() + 2 * G + size_t(i) * (depth + 1);
-        double vals[RW_LAMB_TRUST_DEPTH];
-        std::memcpy(vals, row + 1, sizeof(vals));
-        if ((st = rw_state_set_saved_scalars(s, i, vals, static_cast<uint32_t>(row[0]), stream))) return st;
-      }
-  }
+  if ((st = replicate_meta(c, s, h, root, mk, stream))) return st;
   if ((st = order_after(cs, c->stream))) return st;
   if (bytes_out) *bytes_out = bytes;
   return RW_OK;

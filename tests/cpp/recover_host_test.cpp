@@ -213,7 +213,7 @@ static std::vector<uint32_t> gather_u32(rw_comm* c, uint32_t mine) {
 }
 
 // ------------------------------------------------------------- replication
-static int run_replication(int rank, int n, const void* id, bool big) {
+static int run_replication(int rank, int n, const void* id, bool big, uint32_t flags) {
   CU(cudaSetDevice(rank));
   rw_comm* c = nullptr;
   CK(rw_comm_init(&c, id, n, rank, rank));
@@ -246,11 +246,19 @@ static int run_replication(int rank, int n, const void* id, bool big) {
   CU(cudaDeviceSynchronize());
   cudaStream_t s;
   CU(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  // warm-up exchange (connections), then the timed recovery
+  // warm-up exchange (connections, and for the chain the IPC mappings, which a
+  // communicator keeps), then the timed recovery
   {
     rw_resolution w{};
     std::vector<uint8_t> a(G);
     CK(rw_resolve(rank == 0 ? f.st : nullptr, &h, c, RW_POLICY_UNDO, nullptr, rank == 0 ? a.data() : nullptr, &w, s));
+    std::vector<uint8_t> none(G, 0);  // transfers without undo: the survivor's state is left as it is
+    uint64_t wb = 0;
+    for (int w = 0; w < 3; ++w) {
+      CK(rw_recover_replication(f.st, &h, c, 0, rank == 0 ? none.data() : nullptr, RW_STRATEGY_NONE, flags, 16, s,
+                                &wb));
+      CU(cudaStreamSynchronize(s));
+    }
   }
   const auto t0 = Clock::now();
   std::vector<uint8_t> acts(G, 0);
@@ -259,7 +267,7 @@ static int run_replication(int rank, int n, const void* id, bool big) {
                 s));
   const double t_resolve = ms_since(t0);
   uint64_t bytes = 0;
-  CK(rw_recover_replication(f.st, &h, c, 0, rank == 0 ? acts.data() : nullptr, res.strategy, 0, 16, s, &bytes));
+  CK(rw_recover_replication(f.st, &h, c, 0, rank == 0 ? acts.data() : nullptr, res.strategy, flags, 16, s, &bytes));
   CU(cudaStreamSynchronize(s));
   const double t_total = ms_since(t0);
   EXPECT(res.strategy == RW_STRATEGY_UNDO && res.target == 10, "plan %d target %llu", res.strategy,
@@ -276,9 +284,10 @@ static int run_replication(int rank, int n, const void* id, bool big) {
   for (int r = 1; r < n; ++r)
     EXPECT(all_x[r] == all_x[0] && all_m[r] == all_m[0] && all_v[r] == all_v[0], "rank %d CRC differs", r);
   if (rank == 0)
-    std::printf("PASS replication n=%d groups=%u bytes_per_replacement=%llu resolve_ms=%.3f recovery_ms=%.3f "
+    std::printf("PASS replication%s n=%d groups=%u bytes_per_replacement=%llu resolve_ms=%.3f recovery_ms=%.3f "
                 "(%.1f GB/s per replacement)\n",
-                n, G, (unsigned long long)bytes, t_resolve, t_total, bytes / (t_total * 1e-3) / 1e9);
+                (flags & RW_RECOVER_CHAIN) ? " (copy-engine chain)" : "", n, G, (unsigned long long)bytes,
+                t_resolve, t_total, bytes / (t_total * 1e-3) / 1e9);
   free_flat(f);
   CK(rw_comm_destroy(c));
   return g_fail ? 1 : 0;
@@ -539,12 +548,17 @@ static int run_failure(int rank, int n, const void* id, const std::string& dir, 
 
 int main(int argc, char** argv) {
   if (argc < 3) {
-    std::printf("usage: %s replication|replay|failure <nranks> [gpt2xl]\n", argv[0]);
+    std::printf("usage: %s replication|replay|failure <nranks> [gpt2xl] [chain]\n", argv[0]);
     return 2;
   }
   const std::string what = argv[1];
   const int n = std::atoi(argv[2]);
-  const bool big = argc > 3 && std::string(argv[3]) == "gpt2xl";
+  bool big = false;
+  uint32_t rflags = 0;
+  for (int a = 3; a < argc; ++a) {
+    if (std::string(argv[a]) == "gpt2xl") big = true;
+    if (std::string(argv[a]) == "chain") rflags |= RW_RECOVER_CHAIN;
+  }
   unsigned char id[128];
   if (rw_nccl_unique_id(id)) {  // no CUDA context is created before fork
     std::printf("FAIL ncclGetUniqueId: %s\n", rw_last_error_message());
@@ -558,7 +572,7 @@ int main(int argc, char** argv) {
     if (p == 0) {
       g_rank = r;
       int rc = 0;
-      if (what == "replication") rc = run_replication(r, n, id, big);
+      if (what == "replication") rc = run_replication(r, n, id, big, rflags);
       else if (what == "replay") rc = run_replay(r, n, id);
       else if (what == "failure") rc = run_failure(r, n, id, dir, false);
       std::fflush(stdout);

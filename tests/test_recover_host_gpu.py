@@ -23,9 +23,12 @@ def _run(*args, timeout=600):
 
 
 @need2
+@pytest.mark.parametrize("mode", ["nccl", "chain"])
 @pytest.mark.parametrize("n", sorted({2, min(NGPU, 4)}))
-def test_cpp_replication(n):
-    print(_run("replication", n))
+def test_cpp_replication(n, mode):
+    """Pipelined undo + NCCL broadcasts, or the copy-engine chain
+    (RW_RECOVER_CHAIN): every replica's CRC equals the survivor's."""
+    print(_run("replication", n, *(["chain"] if mode == "chain" else [])))
 
 
 @need2
