@@ -14,6 +14,7 @@ logic.  The per-group decisions are made by the C++ resolver
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Sequence
@@ -359,14 +360,16 @@ def prepare_transfer(state, include_grad: bool = False, group=None) -> None:
 
 
 def recover_replication_pipelined(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = False,
-                                  group=None, pieces: int = 4) -> int:
+                                  group=None, pieces: int = 4, lead: int = 0) -> int:
     """apply_undo + recover_replication as a two-stage pipeline over `pieces`
     contiguous runs of groups: the survivor undoes run i on its stream while
     NCCL broadcasts the already-resolved run i-1 (async broadcasts of buffer
     views; NCCL's kernels co-reside with the memory-bound undo kernel), so the
     undo hides behind the transfer for any number of replacements.  Every rank
     derives the same runs from the shared layout.  Returns bytes per
-    replacement."""
+    replacement.  lead > 0 paces the survivor's undo: run i starts only once the
+    broadcasts of run i - lead are done (an undo burst at full HBM bandwidth
+    slows the transfers it overlaps)."""
     if not (dist.is_available() and dist.is_initialized()):
         raise RwError(17, "NoReplica: no process group")
     rank = dist.get_rank(group)
@@ -388,11 +391,14 @@ def recover_replication_pipelined(state, hyper, plan: ResolvePlan, src: int, inc
             start = i + 1
     comms = _buffer_comms(len(names), group)  # x, m, v transfers run concurrently
     works = []
-    for g0, g1 in runs:
+    for k, (g0, g1) in enumerate(runs):
         lo, hi = state.offsets[g0], state.offsets[g1 - 1] + state.sizes[g1 - 1]
         if rank == src:
             ids = [i for i in range(g0, g1) if i in undo]
             if ids:
+                if lead and k >= lead:
+                    for w in works[(k - lead) * len(names):(k - lead + 1) * len(names)]:
+                        w.wait()  # stream-side: the current stream waits for those broadcasts
                 state.undo(hyper, ids)
         for n, cg in zip(names, comms):
             gsrc = dist.get_global_rank(cg, src) if group is not None else src
@@ -411,6 +417,8 @@ def recover_replication_pipelined(state, hyper, plan: ResolvePlan, src: int, inc
 
 
 _CE_CHAINS: dict = {}
+# (pieces, lead) of the pipelined transfer recover() uses; RW_PIPE="pieces,lead" overrides (sweeps)
+_PIPE = tuple(int(v) for v in os.environ.get("RW_PIPE", "4,0").split(","))
 
 
 def _runs_of(state, pieces: int) -> list[tuple[int, int]]:
@@ -541,7 +549,8 @@ def recover(state, hyper, plan: ResolvePlan, src: int, include_grad: bool = Fals
     if transfer == "fused":
         return transfer, recover_replication_fused(state, hyper, plan, src, include_grad, group)
     if transfer == "pipelined":
-        return transfer, recover_replication_pipelined(state, hyper, plan, src, include_grad, group)
+        return transfer, recover_replication_pipelined(state, hyper, plan, src, include_grad, group,
+                                                       pieces=_PIPE[0], lead=_PIPE[1])
     if transfer == "chain":
         return transfer, recover_replication_chain(state, hyper, plan, src, include_grad, group)
     if dist.get_rank(group) == src:
