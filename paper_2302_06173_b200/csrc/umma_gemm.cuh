@@ -551,7 +551,7 @@ constexpr int kGroupM = RWB_GROUP_M;
 // MH = 1 (8 pair tiles of 256 rows); 4096 rows = 8 pair tiles of 512 for MH = 2
 // (profiles/r02/gemm_variants7_wide.log, replay ms: 1024 / 2048 / 4096 rows -> 633-634 / 627-630 / 623-626)
 template <int MH>
-constexpr int group_tiles2() {
+__host__ __device__ constexpr int group_tiles2() {
   return MH == 1 ? kGroupM / 2 : 8;
 }
 

@@ -29,7 +29,7 @@ __global__ void fill(__nv_bfloat16* p, size_t n, uint32_t seed, float scale) {
   }
 }
 
-template <bool PAIR, int AM, int BMJ, int EPI>
+template <bool PAIR, int AM, int BMJ, int EPI, int MH = 1>
 void probe(const char* name, int M, int N, int K, double secs) {
   __nv_bfloat16 *A, *B, *O, *Y;
   float* bias;
@@ -45,7 +45,7 @@ void probe(const char* name, int M, int N, int K, double secs) {
   EpiArgs ep{O, N, bias, Y, N};
   const int64_t lda = AM == K_MAJOR ? K : M, ldb = BMJ == K_MAJOR ? K : N;
   auto run = [&] {
-    return PAIR ? launch2<256, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, 0)
+    return PAIR ? launch2<256, AM, BMJ, EPI, MH>(A, lda, B, ldb, M, N, K, ep, 0)
                 : launch<256, AM, BMJ, EPI>(A, lda, B, ldb, M, N, K, ep, 0);
   };
   run();
@@ -85,12 +85,13 @@ void probe(const char* name, int M, int N, int K, double secs) {
     for (int j = 0; j < 3; ++j) s[j] += z[i][j];
   }
   for (int i = 0; i < 148; ++i) s[3] += z[i][3];
-  const double tiles = PAIR ? double((M + 255) / 256) * ((N + 255) / 256) : double((M + 127) / 128) * ((N + 255) / 256);
-  const double instr = tiles * ((K + 63) / 64) * 4 / nl;
+  const int pm = 256 * MH;
+  const double tiles = PAIR ? double((M + pm - 1) / pm) * ((N + 255) / 256) : double((M + 127) / 128) * ((N + 255) / 256);
+  const double instr = tiles * ((K + 63) / 64) * 4 * MH / nl;  // per-SM MMA instructions (pair: M256 each)
   const double loop = s[2] / nl;
   printf("%-6s %-28s sustained %7.1f TFLOP/s (%d launches, %.3f ms each) | last %.3f ms: %.1f cyc/MMA (ideal 128), "
          "wait_full %.1f%%, wait_tempty %.1f%%, producer wait_empty %.1f%%, SM clock ~%.0f MHz, %.3f TF/MHz %s\n",
-         PAIR ? "PAIR" : "single", name, tf, n, ms / n, ms1, loop / instr, 100 * s[0] / nl / loop,
+         PAIR ? (MH == 2 ? "WIDE" : "PAIR") : "single", name, tf, n, ms / n, ms1, loop / instr, 100 * s[0] / nl / loop,
          100 * s[1] / nl / loop, 100 * s[3] / 148 / loop, loop / (ms1 * 1e3),
          2.0 * M * N * K / (ms1 * 1e-3) / 1e12 / (loop / (ms1 * 1e3)), err ? cudaGetErrorString(err) : "");
   cudaFree(A);
@@ -103,6 +104,9 @@ void probe(const char* name, int M, int N, int K, double secs) {
 int main(int argc, char** argv) {
   setvbuf(stdout, NULL, _IONBF, 0);
   const double secs = argc > 1 ? atof(argv[1]) : 2.0;
+  probe<true, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16, 2>("forward 16384x16384x4096", 16384, 16384, 4096, secs);
+  probe<true, K_MAJOR, K_MAJOR, EPI_DTANH_BF16, 2>("dgrad 16384x16384x4096", 16384, 16384, 4096, secs);
+  probe<true, MN_MAJOR, MN_MAJOR, EPI_F32_ACC, 2>("wgrad 4096x16384x16384", 4096, 16384, 16384, secs);
   probe<false, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward 16384x16384x4096", 16384, 16384, 4096, secs);
   probe<true, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward 16384x16384x4096", 16384, 16384, 4096, secs);
   probe<false, K_MAJOR, K_MAJOR, EPI_DTANH_BF16>("dgrad 16384x4096x16384", 16384, 4096, 16384, secs);
