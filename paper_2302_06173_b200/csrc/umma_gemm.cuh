@@ -201,6 +201,21 @@ __device__ __forceinline__ void tmem_ld_32cols(uint32_t taddr, float* v) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// the same load without the wait: several loads share one tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld_32cols_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // UMMA shared-memory descriptor (SM100 "version 1"), SWIZZLE_128B.
 //   K-major : rows of 128 B (64 bf16 of K); 8-row groups 1024 B apart (SBO).
 //   MN-major: rows of 128 B (64 bf16 of M/N) per K index; 8 K-rows = 1024 B
@@ -393,6 +408,18 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, int n0, i
 // edge), while the other box is being filled.  Epilogues with an input tile
 // (y of the dtanh epilogues, the old output of the fp32 accumulate) TMA-load
 // it into the box one box ahead and compute in place.
+#ifdef RWB_PAIR_EXPERIMENT
+// epilogue probe (warp 4, lane 0 of every CTA): [0] cycles inside the tile
+// epilogues, [1] waiting for a staging buffer / input box, [2] TMEM loads,
+// [3] column sums
+__device__ long long g_epi_dbg[148][4];
+#define RWB_EPI_T(v) const long long v = (threadIdx.x == 128 ? clock64() : 0)
+#define RWB_EPI_ADD(k, t0) \
+  if (threadIdx.x == 128) g_epi_dbg[blockIdx.x][k] += clock64() - (t0)
+#else
+#define RWB_EPI_T(v)
+#define RWB_EPI_ADD(k, t0)
+#endif
 constexpr uint32_t kEpiBoxBytes = 32 * 128;
 constexpr uint32_t kEpiSmem = 4 * 2 * kEpiBoxBytes;  // 4 warps x double buffer
 
@@ -411,11 +438,13 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
   constexpr int COLS = epi_f32(EPI) ? 32 : 64;
   constexpr int NB = BN / COLS;
   const uint32_t lane = threadIdx.x & 31u;
+  RWB_EPI_T(te0);
 #pragma unroll 1
   for (int i = 0; i < NB; ++i, ++seq) {
     const uint32_t b = seq & 1u;
     uint8_t* buf = ebuf + b * kEpiBoxBytes;
     const int c0 = n0 + i * COLS;
+    RWB_EPI_T(tw0);
     if constexpr (epi_input(EPI)) {
       if (i + 1 < NB && lane == 0) {  // next box's input, into the other buffer once its store has read it
         bulk_wait_read<0>();
@@ -426,10 +455,19 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
       if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read it
       __syncwarp();
     }
+    RWB_EPI_ADD(1, tw0);
+    RWB_EPI_T(tl0);
+    // the box's accumulator columns: every 32-column load issued, one wait
+    uint32_t vr[COLS / 32][32];
+#pragma unroll
+    for (int h = 0; h < COLS / 32; ++h) tmem_ld_32cols_nowait(tbase + uint32_t(i * COLS + h * 32), vr[h]);
+    tmem_wait_ld();
+    RWB_EPI_ADD(2, tl0);
 #pragma unroll
     for (int h = 0; h < COLS / 32; ++h) {
       float v[32];
-      tmem_ld_32cols(tbase + uint32_t(i * COLS + h * 32), v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[h][j]);
       if constexpr (epi_f32(EPI)) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -501,6 +539,7 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
     }
     fence_proxy_async_smem();
     __syncwarp();
+    RWB_EPI_T(tc0);
     if constexpr (uses_y(EPI)) {
       // (a box wholly below the matrix -- the tail of a 256 / 512-row tile -- has no
       // partial row to write: the buffer holds ceil(M / 32) of them)
@@ -523,11 +562,13 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
         }
       }
     }
+    RWB_EPI_ADD(3, tc0);
     if (lane == 0) {
       tma_store_2d(mo, buf, c0, r0);
       bulk_commit();
     }
   }
+  RWB_EPI_ADD(0, te0);
 }
 
 // Grouped tile rasterization: consecutive tile ids walk GM M-tiles down one

@@ -70,6 +70,9 @@ void probe(const char* name, int M, int N, int K, double secs) {
   // one instrumented launch, still hot
   long long z[148][4] = {};
   cudaMemcpyToSymbol(g_pair_dbg, z, sizeof(z));
+#ifdef RWB_PAIR_EXPERIMENT
+  cudaMemcpyToSymbol(g_epi_dbg, z, sizeof(z));
+#endif
   cudaEventRecord(e0);
   run();
   cudaEventRecord(e1);
@@ -77,6 +80,13 @@ void probe(const char* name, int M, int N, int K, double secs) {
   float ms1;
   cudaEventElapsedTime(&ms1, e0, e1);
   cudaMemcpyFromSymbol(z, g_pair_dbg, sizeof(z));
+  long long ze[148][4] = {};
+#ifdef RWB_PAIR_EXPERIMENT
+  cudaMemcpyFromSymbol(ze, g_epi_dbg, sizeof(ze));
+#endif
+  double es[4] = {};
+  for (int i = 0; i < 148; ++i)
+    for (int j = 0; j < 4; ++j) es[j] += ze[i][j];
   double s[4] = {};
   int nl = 0;
   const int step = PAIR ? 2 : 1;
@@ -94,6 +104,10 @@ void probe(const char* name, int M, int N, int K, double secs) {
          PAIR ? (MH == 2 ? "WIDE" : "PAIR") : "single", name, tf, n, ms / n, ms1, loop / instr, 100 * s[0] / nl / loop,
          100 * s[1] / nl / loop, 100 * s[3] / 148 / loop, loop / (ms1 * 1e3),
          2.0 * M * N * K / (ms1 * 1e-3) / 1e12 / (loop / (ms1 * 1e3)), err ? cudaGetErrorString(err) : "");
+  if (es[0] > 0)
+    printf("       epilogue (warp 4): %.0f cycles per CTA; waiting for buffers / input %.1f%%, TMEM loads %.1f%%, "
+           "column sums %.1f%%\n",
+           es[0] / 148, 100 * es[1] / es[0], 100 * es[2] / es[0], 100 * es[3] / es[0]);
   cudaFree(A);
   cudaFree(B);
   cudaFree(O);
