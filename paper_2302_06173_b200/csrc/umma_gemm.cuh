@@ -431,58 +431,101 @@ __device__ __forceinline__ void epi_load_box(const CUtensorMap* mi, uint8_t* buf
   tma_load_2d(buf, mi, bar, c0, r0);
 }
 
-template <int BN, int EPI>
+// `release` runs once, right after the tile's last TMEM load has completed:
+// the accumulator goes back to the MMA warp while the last box is still being
+// computed and stored (TMEM is full for the wide pair, so that box's math and
+// store would otherwise stall the next tile's MMAs).
+// NBUF staging boxes per warp: 2 = the next input box is prefetched into the
+// other buffer and a box's store overlaps the next box's math; 1 = the wide
+// pair's 16-warp epilogue (half the smem per warp) -- an output-only box is
+// computed into registers before the wait for the previous store to have read
+// the buffer, and an input box is fetched once that store has read it.
+#ifndef RWB_EPI_EARLY_RELEASE
+#define RWB_EPI_EARLY_RELEASE 1
+#endif
+template <int NBUF>
+__device__ __forceinline__ void epi_first_input(const CUtensorMap* mi, uint8_t* ebuf, uint64_t* ebar, uint32_t seq,
+                                                int c0, int r0) {
+  const uint32_t b = NBUF == 2 ? (seq & 1u) : 0u;
+  bulk_wait_read<0>();
+  epi_load_box(mi, ebuf + b * kEpiBoxBytes, &ebar[b], c0, r0);
+}
+template <int BN, int EPI, int NBUF, class Release>
 __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0, int M, int N, const EpiArgs& ep,
                                                   const CUtensorMap* mo, const CUtensorMap* mi, uint8_t* ebuf,
-                                                  uint64_t* ebar, uint32_t& seq) {
+                                                  uint64_t* ebar, uint32_t& seq, Release release) {
+  static_assert(NBUF == 1 || NBUF == 2, "one or two staging boxes per warp");
   constexpr int COLS = epi_f32(EPI) ? 32 : 64;
   constexpr int NB = BN / COLS;
   const uint32_t lane = threadIdx.x & 31u;
   RWB_EPI_T(te0);
 #pragma unroll 1
   for (int i = 0; i < NB; ++i, ++seq) {
-    const uint32_t b = seq & 1u;
+    const uint32_t b = NBUF == 2 ? (seq & 1u) : 0u;
     uint8_t* buf = ebuf + b * kEpiBoxBytes;
     const int c0 = n0 + i * COLS;
-    RWB_EPI_T(tw0);
-    if constexpr (epi_input(EPI)) {
-      if (i + 1 < NB && lane == 0) {  // next box's input, into the other buffer once its store has read it
-        bulk_wait_read<0>();
-        epi_load_box(mi, ebuf + (b ^ 1u) * kEpiBoxBytes, &ebar[b ^ 1u], c0 + COLS, r0);
-      }
-      mbar_wait(&ebar[b], (seq >> 1) & 1u);
-    } else {
-      if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read it
-      __syncwarp();
-    }
-    RWB_EPI_ADD(1, tw0);
     RWB_EPI_T(tl0);
     // the box's accumulator columns: every 32-column load issued, one wait
     uint32_t vr[COLS / 32][32];
 #pragma unroll
     for (int h = 0; h < COLS / 32; ++h) tmem_ld_32cols_nowait(tbase + uint32_t(i * COLS + h * 32), vr[h]);
-    tmem_wait_ld();
     RWB_EPI_ADD(2, tl0);
-#pragma unroll
-    for (int h = 0; h < COLS / 32; ++h) {
-      float v[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[h][j]);
-      if constexpr (epi_f32(EPI)) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4* p = reinterpret_cast<float4*>(buf + swz(lane, q));
-          float4 w = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          if constexpr (EPI == EPI_F32_ACC) {
-            const float4 o = *p;
-            w.x = __fadd_rn(o.x, w.x);
-            w.y = __fadd_rn(o.y, w.y);
-            w.z = __fadd_rn(o.z, w.z);
-            w.w = __fadd_rn(o.w, w.w);
+    RWB_EPI_T(tw0);
+    if constexpr (epi_input(EPI)) {
+      if (lane == 0) {
+        if constexpr (NBUF == 2) {
+          if (i + 1 < NB) {  // next box's input, into the other buffer once its store has read it
+            bulk_wait_read<0>();
+            epi_load_box(mi, ebuf + (b ^ 1u) * kEpiBoxBytes, &ebar[b ^ 1u], c0 + COLS, r0);
           }
-          *p = w;
+        } else if (i > 0) {  // this box's input, once the previous box's store has read the buffer
+          bulk_wait_read<0>();
+          epi_load_box(mi, buf, &ebar[0], c0, r0);
         }
-      } else {
+      }
+      mbar_wait(&ebar[b], NBUF == 2 ? (seq >> 1) & 1u : seq & 1u);
+    }
+    RWB_EPI_ADD(1, tw0);
+    tmem_wait_ld();
+    if (RWB_EPI_EARLY_RELEASE && i == NB - 1) {
+      tc_fence_before();
+      __syncwarp();
+      release();
+    }
+    // an output-only box is computed into registers first; the wait for its
+    // buffer (the store two boxes back, or the previous one when NBUF == 1)
+    // comes after the math
+    const auto own_buffer = [&] {
+      if constexpr (!epi_input(EPI)) {
+        RWB_EPI_T(tb0);
+        if (lane == 0) bulk_wait_read<NBUF - 1>();
+        __syncwarp();
+        RWB_EPI_ADD(1, tb0);
+      }
+    };
+    if constexpr (epi_f32(EPI)) {
+      if constexpr (EPI != EPI_F32_ACC) own_buffer();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4* p = reinterpret_cast<float4*>(buf + swz(lane, q));
+        float4 w = make_float4(__uint_as_float(vr[0][4 * q]), __uint_as_float(vr[0][4 * q + 1]),
+                               __uint_as_float(vr[0][4 * q + 2]), __uint_as_float(vr[0][4 * q + 3]));
+        if constexpr (EPI == EPI_F32_ACC) {
+          const float4 o = *p;
+          w.x = __fadd_rn(o.x, w.x);
+          w.y = __fadd_rn(o.y, w.y);
+          w.z = __fadd_rn(o.z, w.z);
+          w.w = __fadd_rn(o.w, w.w);
+        }
+        *p = w;
+      }
+    } else {
+      uint4 pk[COLS / 32][4];
+#pragma unroll
+      for (int h = 0; h < COLS / 32; ++h) {
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(vr[h][j]);
         const int col = c0 + h * 32;
         float w[32];
         if constexpr (EPI == EPI_BIAS_TANH_BF16) {
@@ -524,17 +567,26 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          uint4 pk;
           __nv_bfloat162 h0 = __floats2bfloat162_rn(w[8 * q], w[8 * q + 1]);
           __nv_bfloat162 h1 = __floats2bfloat162_rn(w[8 * q + 2], w[8 * q + 3]);
           __nv_bfloat162 h2 = __floats2bfloat162_rn(w[8 * q + 4], w[8 * q + 5]);
           __nv_bfloat162 h3 = __floats2bfloat162_rn(w[8 * q + 6], w[8 * q + 7]);
-          pk.x = *reinterpret_cast<uint32_t*>(&h0);
-          pk.y = *reinterpret_cast<uint32_t*>(&h1);
-          pk.z = *reinterpret_cast<uint32_t*>(&h2);
-          pk.w = *reinterpret_cast<uint32_t*>(&h3);
-          *reinterpret_cast<uint4*>(buf + swz(lane, h * 4 + q)) = pk;
+          pk[h][q].x = *reinterpret_cast<uint32_t*>(&h0);
+          pk[h][q].y = *reinterpret_cast<uint32_t*>(&h1);
+          pk[h][q].z = *reinterpret_cast<uint32_t*>(&h2);
+          pk[h][q].w = *reinterpret_cast<uint32_t*>(&h3);
         }
+        if constexpr (uses_y(EPI)) {  // in place over the consumed y pieces
+#pragma unroll
+          for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(buf + swz(lane, h * 4 + q)) = pk[h][q];
+        }
+      }
+      if constexpr (!uses_y(EPI)) {
+        own_buffer();
+#pragma unroll
+        for (int h = 0; h < COLS / 32; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(buf + swz(lane, h * 4 + q)) = pk[h][q];
       }
     }
     fence_proxy_async_smem();
@@ -567,6 +619,11 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
       tma_store_2d(mo, buf, c0, r0);
       bulk_commit();
     }
+  }
+  if (!RWB_EPI_EARLY_RELEASE) {
+    tc_fence_before();
+    __syncwarp();
+    release();
   }
   RWB_EPI_ADD(0, te0);
 }
@@ -802,18 +859,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (true) {  // probe only: release the accumulator without reading it
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
+        if (lane == 0 && ep.tma_epi) mbar_arrive(&tempty_bar[acc]);
       } else
 #endif
       if (ep.tma_epi) {
         if constexpr (epi_input(EPI)) {  // the tile's first input box overlaps the wait
-          if (lane == 0) {
-            bulk_wait_read<0>();
-            epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], n0, m0 + ew * 32);
-          }
+          if (lane == 0) epi_first_input<2>(&tma_i, ebuf, ebar, seq, n0, m0 + ew * 32);
         }
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
-        epilogue_tile_tma<BN, EPI>(tbase, m0 + ew * 32, n0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+        epilogue_tile_tma<BN, EPI, 2>(tbase, m0 + ew * 32, n0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq, [&] {
+          if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        });
       } else {
         YChunk y0;
         if constexpr (uses_y(EPI)) load_y_chunk(ep, row, n0, M, N, y0);  // overlaps the wait
@@ -821,9 +878,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         epilogue_tile<BN, EPI>(tbase, row, n0, M, N, ep, &y0);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (!ep.tma_epi) {  // (the TMA epilogue released the accumulator after its last TMEM load)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -913,11 +972,16 @@ struct Cfg2 {
   static constexpr int kCQ = MH == 2 ? RWB_GEMM2_CQ : 1;  // column slices per half (warps per lane quarter)
   static constexpr int kEpiWarps = 4 * MH * kCQ;
   static constexpr int kThreads = 128 + 32 * kEpiWarps;
-  static constexpr uint32_t kEpiSmemT = kEpiWarps * 2 * kEpiBoxBytes;
+  // sixteen epilogue warps (kCQ = 2) stage one box each, so three stages still fit
+#ifndef RWB_GEMM2_EPIBUFS
+#define RWB_GEMM2_EPIBUFS (RWB_GEMM2_CQ == 2 ? 1 : 2)
+#endif
+  static constexpr int kEpiBufs = MH == 2 ? RWB_GEMM2_EPIBUFS : 2;
+  static constexpr uint32_t kEpiSmemT = kEpiWarps * kEpiBufs * kEpiBoxBytes;
 #ifdef RWB_GEMM2_STAGES
   static constexpr int kStages = RWB_GEMM2_STAGES;
 #else
-  static constexpr int kStages = (MH == 1 ? 6 : (kCQ == 1 ? 3 : 2)) * (64 / BK);
+  static constexpr int kStages = (MH == 1 ? 6 : (kEpiWarps * kEpiBufs <= 16 ? 3 : 2)) * (64 / BK);
 #endif
   static constexpr uint32_t kHalfBytes = BM * BK * 2;      // 16 KB: 128 rows of A
   static constexpr uint32_t kABytes = MH * kHalfBytes;     // this CTA's MH x 128 rows
@@ -1109,7 +1173,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
     const int cq = (ewg >> 2) / MH;     // its column slice of the half (kCQ slices)
     constexpr int BNQ = BN / C::kCQ;
     const uint32_t tempty_leader = mapa_rank0(smem_u32(&tempty_bar[0]));
-    uint8_t* ebuf = smem + S * C::kStageBytes + ewg * 2 * kEpiBoxBytes;
+    uint8_t* ebuf = smem + S * C::kStageBytes + ewg * C::kEpiBufs * kEpiBoxBytes;
     uint64_t* ebar = &epi_bar[ewg * 2];
     uint32_t seq = 0;
     int acc = 0;
@@ -1125,14 +1189,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
         const uint32_t tbase = tmem_base + (uint32_t(ew * 32) << 16) + uint32_t((acc * MH + h) * BN + cq * BNQ);
         if (ep.tma_epi) {
           if constexpr (epi_input(EPI)) {
-            if (lane == 0) {
-              bulk_wait_read<0>();
-              epi_load_box(&tma_i, ebuf + (seq & 1u) * kEpiBoxBytes, &ebar[seq & 1u], c0, r0);
-            }
+            if (lane == 0) epi_first_input<C::kEpiBufs>(&tma_i, ebuf, ebar, seq, c0, r0);
           }
           mbar_wait(&tfull_bar[acc], acc_phase);
           tc_fence_after();
-          epilogue_tile_tma<BNQ, EPI>(tbase, r0, c0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq);
+          epilogue_tile_tma<BNQ, EPI, C::kEpiBufs>(tbase, r0, c0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq, [&] {
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
+          });
         } else {
           YChunk y0;
           if constexpr (uses_y(EPI)) load_y_chunk(ep, row, c0, M, N, y0);
@@ -1141,9 +1204,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
           epilogue_tile<BNQ, EPI>(tbase, row, c0, M, N, ep, &y0);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
+      if (!ep.tma_epi) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
+      }
       if (++acc == NACC) {
         acc = 0;
         acc_phase ^= 1;

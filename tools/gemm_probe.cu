@@ -121,6 +121,7 @@ int main(int argc, char** argv) {
   probe<true, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16, 2>("forward 16384x16384x4096", 16384, 16384, 4096, secs);
   probe<true, K_MAJOR, K_MAJOR, EPI_DTANH_BF16, 2>("dgrad 16384x16384x4096", 16384, 16384, 4096, secs);
   probe<true, MN_MAJOR, MN_MAJOR, EPI_F32_ACC, 2>("wgrad 4096x16384x16384", 4096, 16384, 16384, secs);
+  if (argc > 2 && argv[2][0] == 'w') return 0;  // "wide": the MH = 2 kernels only
   probe<false, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward 16384x16384x4096", 16384, 16384, 4096, secs);
   probe<true, K_MAJOR, MN_MAJOR, EPI_BIAS_TANH_BF16>("forward 16384x16384x4096", 16384, 16384, 4096, secs);
   probe<false, K_MAJOR, K_MAJOR, EPI_DTANH_BF16>("dgrad 16384x4096x16384", 16384, 4096, 16384, secs);
