@@ -544,7 +544,13 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
             for (int j = 0; j < 32; ++j) bv[j] = (col + j < N) ? __ldg(ep.bias + col + j) : 0.f;
           }
 #pragma unroll
-          for (int j = 0; j < 32; ++j) w[j] = tanh_fast(__fadd_rn(v[j], bv[j]));
+          for (int j = 0; j < 32; ++j) {
+#ifdef RWB_PROBE_NOTANH  // probe only: the epilogue without its MUFU work
+            w[j] = __fadd_rn(v[j], bv[j]);
+#else
+            w[j] = tanh_fast(__fadd_rn(v[j], bv[j]));
+#endif
+          }
         } else if constexpr (uses_y(EPI)) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -583,6 +589,9 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
       }
       if constexpr (!uses_y(EPI)) {
         own_buffer();
+#ifdef RWB_PROBE_NOSTS  // probe only: no staging writes (the stores send stale smem)
+        if (lane == 32)
+#endif
 #pragma unroll
         for (int h = 0; h < COLS / 32; ++h)
 #pragma unroll
@@ -920,8 +929,21 @@ __device__ __forceinline__ uint32_t mapa_rank0(uint32_t local_smem_addr) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local_smem_addr));
   return r;
 }
+// Arrive on a barrier of another CTA of the cluster.  The accumulator-empty
+// signal only orders this warp's completed TMEM loads (tcgen05.wait::ld +
+// fence::before_thread_sync) before the peer's next MMAs: release at CTA
+// scope (the default semantics) suffices -- a cluster-scope release compiles
+// to MEMBAR.ALL.GPU + ERRBAR, which the epilogue warps measurably stall on
+// (ncu source page, profiles/r02/README.md)
+#ifndef RWB_ARRIVE_CLUSTER_RELEASE
+#define RWB_ARRIVE_CLUSTER_RELEASE 0
+#endif
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+#if RWB_ARRIVE_CLUSTER_RELEASE
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
 }
 // TMA load into this CTA's smem, completion counted on the LEADER's barrier
 __device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
