@@ -450,10 +450,37 @@ __device__ __forceinline__ void epi_first_input(const CUtensorMap* mi, uint8_t* 
   bulk_wait_read<0>();
   epi_load_box(mi, ebuf + b * kEpiBoxBytes, &ebar[b], c0, r0);
 }
+// The tile's bias columns [c0, c0 + BN) into this warp's shared array (zero
+// past N), read by the forward epilogue as broadcast LDS instead of global
+// loads on the critical path; staged while the warp waits for the accumulator.
+template <int BN>
+__device__ __forceinline__ void stage_bias(float* sb, const float* bias, int c0, int N) {
+  constexpr int PER = BN / 32;  // columns per lane
+  static_assert(PER % 4 == 0, "float4 pieces");
+  const int lane = int(threadIdx.x & 31u);
+  __syncwarp();  // every lane is done reading the previous tile's bias
+#pragma unroll
+  for (int q = 0; q < PER; q += 4) {
+    const int c = c0 + lane * PER + q;
+    float4 b;
+    if (c + 4 <= N) {
+      b = __ldg(reinterpret_cast<const float4*>(bias + c));
+    } else {
+      b.x = c < N ? __ldg(bias + c) : 0.f;
+      b.y = c + 1 < N ? __ldg(bias + c + 1) : 0.f;
+      b.z = c + 2 < N ? __ldg(bias + c + 2) : 0.f;
+      b.w = c + 3 < N ? __ldg(bias + c + 3) : 0.f;
+    }
+    *reinterpret_cast<float4*>(sb + lane * PER + q) = b;
+  }
+  __syncwarp();
+}
+
 template <int BN, int EPI, int NBUF, class Release>
 __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0, int M, int N, const EpiArgs& ep,
                                                   const CUtensorMap* mo, const CUtensorMap* mi, uint8_t* ebuf,
-                                                  uint64_t* ebar, uint32_t& seq, Release release) {
+                                                  uint64_t* ebar, uint32_t& seq, Release release,
+                                                  const float* sbias = nullptr) {
   static_assert(NBUF == 1 || NBUF == 2, "one or two staging boxes per warp");
   constexpr int COLS = epi_f32(EPI) ? 32 : 64;
   constexpr int NB = BN / COLS;
@@ -530,7 +557,22 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
         float w[32];
         if constexpr (EPI == EPI_BIAS_TANH_BF16) {
           float bv[32];
-          if (col + 32 <= N) {
+#ifdef RWB_PROBE_NOBIAS  // probe only: no bias loads
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bv[j] = float(j) * 0.5f;
+          if (false) {
+#else
+          if (sbias) {  // staged in shared memory at the tile's start (zero past N): broadcast reads
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b4 = *reinterpret_cast<const float4*>(sbias + i * COLS + h * 32 + j);
+              bv[j] = b4.x;
+              bv[j + 1] = b4.y;
+              bv[j + 2] = b4.z;
+              bv[j + 3] = b4.w;
+            }
+          } else if (col + 32 <= N) {
+#endif
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               const float4 b4 = __ldg(reinterpret_cast<const float4*>(ep.bias + col + j));
@@ -540,8 +582,10 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
               bv[j + 3] = b4.w;
             }
           } else {
+#ifndef RWB_PROBE_NOBIAS
 #pragma unroll
             for (int j = 0; j < 32; ++j) bv[j] = (col + j < N) ? __ldg(ep.bias + col + j) : 0.f;
+#endif
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -1011,7 +1055,12 @@ struct Cfg2 {
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr int kNAcc = MH == 1 ? 2 : 1;            // accumulator stages in TMEM
   static constexpr uint32_t kTmemCols = kNAcc * MH * BN;   // 512 either way
-  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmemT + 1024;
+#ifndef RWB_GEMM2_SBIAS
+#define RWB_GEMM2_SBIAS 1
+#endif
+  // per-warp bias columns (the wide kernel has the smem; MH = 1 uses six stages)
+  static constexpr uint32_t kBiasSmem = (RWB_GEMM2_SBIAS && MH == 2) ? kEpiWarps * (BN / kCQ) * 4 : 0;
+  static constexpr size_t kSmem = size_t(kStages) * kStageBytes + kEpiSmemT + kBiasSmem + 1024;
 };
 
 template <int BN, int AMAJ, int BMAJ, int EPI, int MH = 1>
@@ -1213,11 +1262,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Cfg2<BN, MH>::kThrea
           if constexpr (epi_input(EPI)) {
             if (lane == 0) epi_first_input<C::kEpiBufs>(&tma_i, ebuf, ebar, seq, c0, r0);
           }
+          float* sbias = nullptr;
+          if constexpr (EPI == EPI_BIAS_TANH_BF16 && C::kBiasSmem > 0) {
+            sbias = reinterpret_cast<float*>(smem + S * C::kStageBytes + C::kEpiSmemT) + ewg * BNQ;
+            stage_bias<BNQ>(sbias, ep.bias, c0, N);
+          }
           mbar_wait(&tfull_bar[acc], acc_phase);
           tc_fence_after();
           epilogue_tile_tma<BNQ, EPI, C::kEpiBufs>(tbase, r0, c0, M, N, ep, &tma_o, &tma_i, ebuf, ebar, seq, [&] {
             if (lane == 0) mbar_arrive_cluster(tempty_leader + uint32_t(acc) * 8u);
-          });
+          }, sbias);
         } else {
           YChunk y0;
           if constexpr (uses_y(EPI)) load_y_chunk(ep, row, c0, M, N, y0);
