@@ -102,10 +102,14 @@ namespace {
 // wait for completion of the host-side part (not the kernels) while watching
 // the failure flag, so a dead peer can never wedge the host thread.
 int nccl_settle(rw_comm* c, ncclResult_t r, const char* what) {
-  // a host-side operation still in progress after the watch timeout (or 120 s
-  // unwatched) is a failure too: it waits on a peer that is gone
+  // a host-side operation still in progress long after the watch timeout (or
+  // 120 s unwatched) is a failure too: it waits on a peer that is gone.  The
+  // host side of a fresh communicator's first collectives includes NCCL's lazy
+  // connection setup (seconds on some boxes), so it gets at least 30 s; a dead
+  // peer during a collective's device phase is the watchdog's job
+  // (timeout_ms, measured per tracked batch).
   const auto t0 = Clock::now();
-  const double limit = c->timeout_ms ? double(c->timeout_ms) : 120000.0;
+  const double limit = c->timeout_ms ? std::max(double(c->timeout_ms), 30000.0) : 120000.0;
   while (r == ncclInProgress) {
     if (c->failed.load()) return hfail(RW_CHANNEL_BROKEN, "ChannelBroken: %s: communicator failed", what);
     ncclResult_t a = ncclSuccess;
@@ -137,11 +141,19 @@ int nccl_settle(rw_comm* c, ncclResult_t r, const char* what) {
 // the communicator failed (its kernels are then terminated by the shrink /
 // abort that repairs it).
 int sync_comm(rw_comm* c, const char* what) {
+  // unwatched communicators get the same bound as nccl_settle: no completion
+  // in 120 s means a collective waits on a peer that is gone
+  const auto t0 = Clock::now();
   for (;;) {
     const cudaError_t e = cudaStreamQuery(c->stream);
     if (e == cudaSuccess) break;
     if (e != cudaErrorNotReady) return hfail(RW_CUDA_ERROR, "CUDA error in %s: %s", what, cudaGetErrorString(e));
     if (c->failed.load()) return hfail(RW_CHANNEL_BROKEN, "ChannelBroken: %s: peer failure detected", what);
+    if (!c->poll_us && ms_since(t0) > 120000.0) {
+      c->detect_ms = ms_since(t0);
+      c->failed = RW_COMM_FAILED_TIMEOUT;
+      return hfail(RW_CHANNEL_BROKEN, "ChannelBroken: %s: no completion for %.0f ms", what, c->detect_ms);
+    }
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
   if (c->failed.load()) return hfail(RW_CHANNEL_BROKEN, "ChannelBroken: %s: peer failure detected", what);

@@ -415,6 +415,20 @@ static bool read_file(const std::string& p, void* data, size_t n) {
   return got == n;
 }
 
+// waits for a file another rank publishes; a rank that failed before
+// publishing must not leave this one spinning forever
+static bool wait_file(const std::string& p, void* data, size_t n, double limit_ms = 60000.0) {
+  const auto t0 = Clock::now();
+  while (!read_file(p, data, n)) {
+    if (ms_since(t0) > limit_ms) {
+      TRACE("gave up waiting for %s after %.0f ms", p.c_str(), limit_ms);
+      return false;
+    }
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  }
+  return true;
+}
+
 static int run_failure(int rank, int n, const void* id, const std::string& dir, bool replacement) {
   // survivors: ranks 0..n-2; the dying rank n-1; the replacement takes rank n-1 of a new communicator
   const int dev = replacement ? n - 1 : rank;
@@ -425,11 +439,12 @@ static int run_failure(int rank, int n, const void* id, const std::string& dir, 
   rw_membership* mem = nullptr;
   if (replacement) {  // join: wait for the survivors' new unique id, then take over the dead slot
     unsigned char nid[128];
-    while (!read_file(dir + "/join.id", nid, sizeof(nid))) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    if (!wait_file(dir + "/join.id", nid, sizeof(nid))) return 1;
     CK(rw_membership_open(&mem, (dir + "/heartbeats").c_str(), n - 1, n, 2000));
     const auto t0 = Clock::now();
     rw_comm* c = nullptr;
     CK(rw_comm_init(&c, nid, n, n - 1, dev));
+    CK(rw_comm_watch(c, 200, 10000));
     const double join_ms = ms_since(t0);
     TRACE("replacement joined in %.1f ms", join_ms);
     Flat f = make_flat(sizes, dev);
@@ -498,12 +513,12 @@ static int run_failure(int rank, int n, const void* id, const std::string& dir, 
       CK(rw_nccl_unique_id(sid));
       write_file(dir + "/survivors.id", sid, sizeof(sid));
     } else {
-      while (!read_file(dir + "/survivors.id", sid, sizeof(sid)))
-        std::this_thread::sleep_for(std::chrono::milliseconds(1));
+      if (!wait_file(dir + "/survivors.id", sid, sizeof(sid))) return 1;
     }
     CK(rw_comm_init(&sc, sid, n - 1, rank, dev));
   }
   const double shrink_ms = ms_since(t_s);
+  CK(rw_comm_watch(sc, 200, 10000));
   TRACE("survivor communicator (%s) in %.1f ms", repair, shrink_ms);
   CK(rw_comm_abort(c));
   EXPECT(rw_comm_size(sc) == n - 1, "shrunk size %d", rw_comm_size(sc));
@@ -517,12 +532,13 @@ static int run_failure(int rank, int n, const void* id, const std::string& dir, 
   if (rank == 0) {
     CK(rw_nccl_unique_id(nid));
     write_file(dir + "/join.id", nid, sizeof(nid));
-  } else {
-    while (!read_file(dir + "/join.id", nid, sizeof(nid))) std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  } else if (!wait_file(dir + "/join.id", nid, sizeof(nid))) {
+    return 1;
   }
   const auto t_j = Clock::now();
   rw_comm* jc = nullptr;
   CK(rw_comm_init(&jc, nid, n, rank, dev));
+  CK(rw_comm_watch(jc, 200, 10000));
   const double join_ms = ms_since(t_j);
   TRACE("joined in %.1f ms", join_ms);
   rw_resolution r2{};

@@ -16,7 +16,12 @@ need2 = pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs (one NCCL rank per 
 
 
 def _run(*args, timeout=600):
-    out = subprocess.run([BIN, *map(str, args)], capture_output=True, text=True, timeout=timeout)
+    try:
+        out = subprocess.run([BIN, *map(str, args)], capture_output=True, text=True, timeout=timeout)
+    except subprocess.TimeoutExpired as e:  # show how far every rank got
+        def tail(b):
+            return (b.decode(errors="replace") if isinstance(b, bytes) else (b or ""))[-4000:]
+        raise AssertionError(f"timed out after {timeout} s\n{tail(e.stdout)}\n{tail(e.stderr)}") from None
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
     assert "PASS" in out.stdout, out.stdout[-4000:]
     return out.stdout
