@@ -306,7 +306,10 @@ int rw_comm_abort(rw_comm* c);      /* ncclCommAbort + free */
  * poll_us and watches every collective this library enqueued; one that has
  * not completed after timeout_ms (0 = no timeout) marks the communicator
  * failed (fail-stop: the peer is gone).  Host waits inside the library then
- * return RW_CHANNEL_BROKEN instead of blocking. */
+ * return RW_CHANNEL_BROKEN instead of blocking.  A collective's host-side
+ * phase (NCCL's lazy connection setup on a fresh communicator) is allowed
+ * max(timeout_ms, 30 s); without a watch every host wait gives up after
+ * 120 s. */
 enum { RW_COMM_OK = 0, RW_COMM_FAILED_NCCL_ERROR = 1, RW_COMM_FAILED_TIMEOUT = 2 };
 int rw_comm_watch(rw_comm* c, uint32_t poll_us, uint32_t timeout_ms);
 /* reason = RW_COMM_*; detect_ms = age of the stuck collective when detected */
