@@ -692,7 +692,11 @@ def logging_bench(records: int = 16, rows: int = 16384, dim: int = 4096) -> dict
     ts = [synth_inputs(3, 0, i, rows, dim) for i in range(4)]
     d = tempfile.mkdtemp(prefix="rw_log_", dir=root)
     try:
-        lg = Logger(d, machine=0, chunk_records=8, pinned_bytes=1 << 30)
+        # the pinned slab holds one iteration's boundary records (16 x 134 MB), so
+        # log_send never waits for the writers (with 1 GiB the producer blocked
+        # ~85 ms per iteration on backpressure: profiles/r02/logging_slab_lanes.log)
+        pinned = int(os.environ.get("RW_LOG_PINNED_MIB", "2048")) << 20
+        lg = Logger(d, machine=0, chunk_records=8, pinned_bytes=pinned)
         # warm-up record (slab, files, CRC tables)
         lg.log_send(ts[0], 0, 1, 0, 0, 0)
         lg.flush()
