@@ -779,7 +779,7 @@ def checkpoint_bench(sizes, reps: int = 2) -> dict:
         w, l_ = min(wt), min(lt)
         return dict(bytes=nbytes, dir=root, write_s=round(w, 3), write_gbs=round(nbytes / w / 1e9, 2),
                     load_s=round(l_, 3), load_gbs=round(nbytes / l_ / 1e9, 2), bit_exact=bool(ok),
-                    path="native: 8 I/O workers x (32 MiB pinned chunk + copy stream), one part file each, "
+                    path="native: 16 I/O workers x (32 MiB pinned chunk + copy stream), one part file each, "
                          "GPU CRC32, fsync + atomic manifest")
     finally:
         shutil.rmtree(d, ignore_errors=True)
@@ -1279,6 +1279,8 @@ ONLY = {
     "logging_capture": lambda: logging_bench(),
     "config5_sweep": lambda: config5_sweep(),
     "config1_crash": lambda: config1_crash(),
+    "checkpoint": lambda: checkpoint_bench(__import__("paper_2302_06173_b200.workloads", fromlist=["CONFIGS"])
+                                           .CONFIGS["adam340m"]["sizes"]()),
 }
 
 

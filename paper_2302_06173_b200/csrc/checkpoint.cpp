@@ -15,7 +15,7 @@
 // Hence "manifest visible <=> all blobs fully written"; a crash anywhere
 // before the final rename leaves the previous MANIFEST the latest valid one.
 //
-// Data path: device buffers move in 32 MiB chunks through 8 I/O workers,
+// Data path: device buffers move in 32 MiB chunks through 16 I/O workers,
 // each with its own pinned chunk and copy stream (D2H + pwrite / pread +
 // H2D at the chunk's file offset), so PCIe copies, page-cache copies and the
 // storage work in parallel.  Each device blob's CRC32 (the wire.cpp polynomial) is
@@ -55,7 +55,10 @@ int cfail(int code, const std::string& msg) {
   } while (0)
 
 constexpr uint64_t kChunk = 32ull << 20;  // pinned staging chunk per worker
-constexpr int kWorkers = 8;                // I/O threads, each with its own stream + buffer
+#ifndef RW_CKPT_WORKERS
+#define RW_CKPT_WORKERS 16  // = the GPU box's host cores: 27-29 / 30-32 GB/s write / load vs 19-21 / 22-23 with 8
+#endif
+constexpr int kWorkers = RW_CKPT_WORKERS;  // I/O threads, each with its own stream + buffer
 
 // CRC32 (reflected 0xEDB88320), the wire.cpp:31-38 function, for host blobs
 uint32_t crc32_host(const void* p, uint64_t n) {
