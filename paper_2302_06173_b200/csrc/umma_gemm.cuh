@@ -701,9 +701,12 @@ constexpr int kGroupM = RWB_GROUP_M;
 // the pair kernels' raster group in M rows: 16 single-CTA tiles' worth for
 // MH = 1 (8 pair tiles of 256 rows); 4096 rows = 8 pair tiles of 512 for MH = 2
 // (profiles/r02/gemm_variants7_wide.log, replay ms: 1024 / 2048 / 4096 rows -> 633-634 / 627-630 / 623-626)
+#ifndef RWB_GROUP_WIDE
+#define RWB_GROUP_WIDE 8
+#endif
 template <int MH>
 __host__ __device__ constexpr int group_tiles2() {
-  return MH == 1 ? kGroupM / 2 : 8;
+  return MH == 1 ? kGroupM / 2 : RWB_GROUP_WIDE;
 }
 
 template <int BN>
