@@ -264,8 +264,11 @@ __device__ __forceinline__ float tanh_fast(float x) {
 struct YChunk {
   uint4 q[4];
 };
+// (the register epilogue serves pitches / bases the TMA maps reject, so every
+// vector access checks the actual address)
+__device__ __forceinline__ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 __device__ __forceinline__ void load_y_chunk(const EpiArgs& ep, int row, int col0, int M, int N, YChunk& y) {
-  if (row < M && col0 + 32 <= N) {
+  if (row < M && col0 + 32 <= N && al16(ep.y + int64_t(row) * ep.ldy + col0)) {
     const uint4* p = reinterpret_cast<const uint4*>(ep.y + int64_t(row) * ep.ldy + col0);
 #pragma unroll
     for (int q = 0; q < 4; ++q) y.q[q] = __ldg(p + q);
@@ -279,7 +282,7 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
                                           const YChunk* yk = nullptr) {
     if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
       float* o = static_cast<float*>(ep.out) + int64_t(row) * ep.ldo + col0;
-      if (col0 + 32 <= N) {
+      if (col0 + 32 <= N && al16(o)) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4) {
           float4 w = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
@@ -300,10 +303,11 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
     } else {
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(ep.out) + int64_t(row) * ep.ldo + col0;
       const bool full = col0 + 32 <= N;
+      const bool full_y = full && (!uses_y(EPI) || al16(ep.y + int64_t(row) * ep.ldy + col0));
       float w[32];
       if constexpr (EPI == EPI_BIAS_TANH_BF16) {
         float bv[32];
-        if (full) {  // same 128 B for every lane of the warp: one broadcast transaction each
+        if (full && (reinterpret_cast<uintptr_t>(ep.bias) & 15u) == 0) {  // same 128 B for every lane: one broadcast each
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             const float4 b4 = __ldg(reinterpret_cast<const float4*>(ep.bias + col0 + j));
@@ -321,7 +325,7 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
       } else if constexpr (uses_y(EPI)) {
         const __nv_bfloat16* yp = ep.y + int64_t(row) * ep.ldy + col0;
         float yv[32];
-        if (full) {  // 64 contiguous bytes of this row: 4 x 128-bit loads (prefetched when yk)
+        if (full_y) {  // 64 contiguous bytes of this row: 4 x 128-bit loads (prefetched when yk)
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
             const uint4 u = yk ? yk->q[j / 8] : *reinterpret_cast<const uint4*>(yp + j);
@@ -351,7 +355,7 @@ __device__ __forceinline__ void epi_chunk(const float* v, int row, int col0, int
 #ifdef RWB_PROBE_NOSTORE
       if (w[0] != 12345.f) return;  // probe only: compute everything, store (almost) nothing
 #endif
-      if (col0 + 32 <= N) {
+      if (full && al16(o)) {
 #pragma unroll
         for (int j = 0; j < 32; j += 8) {
           uint4 pk;
@@ -458,12 +462,13 @@ __device__ __forceinline__ void stage_bias(float* sb, const float* bias, int c0,
   constexpr int PER = BN / 32;  // columns per lane
   static_assert(PER % 4 == 0, "float4 pieces");
   const int lane = int(threadIdx.x & 31u);
+  const bool vec = (reinterpret_cast<uintptr_t>(bias) & 15u) == 0;  // caller-owned pointer: may be unaligned
   __syncwarp();  // every lane is done reading the previous tile's bias
 #pragma unroll
   for (int q = 0; q < PER; q += 4) {
     const int c = c0 + lane * PER + q;
     float4 b;
-    if (c + 4 <= N) {
+    if (vec && c + 4 <= N) {
       b = __ldg(reinterpret_cast<const float4*>(bias + c));
     } else {
       b.x = c < N ? __ldg(bias + c) : 0.f;
@@ -571,7 +576,7 @@ __device__ __forceinline__ void epilogue_tile_tma(uint32_t tbase, int r0, int n0
               bv[j + 2] = b4.z;
               bv[j + 3] = b4.w;
             }
-          } else if (col + 32 <= N) {
+          } else if (col + 32 <= N && (reinterpret_cast<uintptr_t>(ep.bias) & 15u) == 0) {
 #endif
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {

@@ -1,10 +1,10 @@
 """Replay path on the GPU.
 
 Bars:
-  * forward_stage / backward_stage / mse_loss vs the fp64 reference library:
-    relative tolerance (bf16 tensor-core GEMMs, fp32 accumulation):
-    |gpu - ref| <= 3e-2 * max|ref| per tensor (stated in north_star terms:
-    "replay within a stated relative tolerance");
+  * forward_stage / backward_stage / mse_loss vs the fp64 reference library at
+    desk shapes: |gpu - ref| <= 3e-2 * max|ref| per tensor, a smoke-level bar
+    (the derived per-element bounds at config-4 depth live in
+    tests/test_replay_parity_gpu.py);
   * logging replay == failure-free GPU ghost run, BIT FOR BIT (acceptance 4);
   * parallel recovery (mb mod d, ascending-mb merge) == sequential replay,
     BIT FOR BIT (acceptance 5), d = 2 emulated on one GPU;
@@ -130,6 +130,40 @@ def test_gemm_engines_agree_bitwise(rows, din, dh, dout):
     for other in results[1:]:
         for a, b in zip(results[0], other):
             assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("pair", [0, 2])
+def test_unaligned_outputs_take_the_register_epilogue(pair):
+    """Output / y operands whose base is not 16-byte aligned cannot be TMA
+    tensor-map operands: the GEMMs fall back to the register epilogue, whose
+    vector accesses check the actual addresses.  The last layer's output, the
+    stage-boundary gradient and the previous stage's y at a 2-byte offset give
+    the same bits as aligned buffers."""
+    from paper_2302_06173_b200.replay import LIB
+    from paper_2302_06173_b200._lib import check
+    rows, din, dh, dout = 200, 96, 264, 56
+    check(LIB.rw_replay_set_gemm_engine(1, pair))
+    try:
+        def run(off):
+            st = Stage(3, din, dh, dout, 2, 5, ADAM)
+            prev_a = synth_inputs(5, 0, 9, rows, din)
+            acts = st.new_acts(rows, synth_inputs(5, 0, 0, rows, din))
+            last = torch.empty(rows * dout + 8, dtype=torch.bfloat16, device="cuda")[off:off + rows * dout]
+            acts[-1] = last.view(rows, dout)
+            st.forward(acts)
+            gbuf = torch.empty(rows * din + 8, dtype=torch.bfloat16, device="cuda")[off:off + rows * din]
+            pbuf = torch.empty(rows * din + 8, dtype=torch.bfloat16, device="cuda")[off:off + rows * din]
+            pbuf.copy_(prev_a.reshape(-1))
+            gout, prev = gbuf.view(rows, din), pbuf.view(rows, din)
+            st.backward(acts, synth_inputs(5, 1, 0, rows, dout), gout, accumulate=False, prev_y=prev,
+                        fuse_db=False)
+            torch.cuda.synchronize()
+            return [acts[1].clone(), acts[2].clone(), gout.clone(), st.grad.clone()]
+        aligned, shifted = run(0), run(1)
+        for a, b in zip(aligned, shifted):
+            assert torch.equal(a, b)
+    finally:
+        check(LIB.rw_replay_set_gemm_engine(-1, -1))
 
 
 @pytest.mark.parametrize("rows", [512, 4096, 200])
