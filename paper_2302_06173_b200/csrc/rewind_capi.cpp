@@ -447,6 +447,19 @@ static int state_create(rw_state** out, int32_t dtype, void* x, void* g, void* m
     rw_state_destroy(s);
     return cuda_fail(e, "rw_state_create");
   }
+  // Size every launch slot for a call over all groups now: growing one later
+  // means cudaFreeHost / cudaFree (device-wide synchronisations) inside the
+  // call -- e.g. inside the first recovery of a job, the one that matters.
+  {
+    const uint32_t pre = std::min<uint32_t>(std::max<uint32_t>(n_groups, 1), 4096);
+    for (auto& sl : s->slots) {
+      const int st = ensure_slot(s, sl, pre, pre);
+      if (st) {
+        rw_state_destroy(s);
+        return st;
+      }
+    }
+  }
   *out = s;
   return RW_OK;
 }

@@ -26,6 +26,7 @@
 #include <sys/wait.h>
 #include <unistd.h>
 
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdint>
@@ -222,6 +223,7 @@ static int run_replication(int rank, int n, const void* id, bool big, uint32_t f
   rw_hyper h = adam();
   Flat f = make_flat(sizes, rank);
   Flat expect{};
+  std::array<uint32_t, 3> exp_crc{};
   if (rank == 0) {
     fill_state(f);
     crash(f, h, G / 2);
@@ -242,6 +244,11 @@ static int run_replication(int rank, int n, const void* id, bool big, uint32_t f
     CK(rw_apply_resolution(expect.st, &h, acts.data(), strat, nullptr, nullptr));
     CU(cudaDeviceSynchronize());
     (void)rs;
+    // keep only its CRCs: a second resident copy of the state would also crowd
+    // the survivor's address translation during the timed transfer
+    const uint64_t nbe = expect.total * 4;
+    exp_crc = {crc_of(expect.x, nbe), crc_of(expect.m, nbe), crc_of(expect.v, nbe)};
+    free_flat(expect);
   }
   CU(cudaDeviceSynchronize());
   cudaStream_t s;
@@ -275,9 +282,7 @@ static int run_replication(int rank, int n, const void* id, bool big, uint32_t f
   const uint64_t nb = f.total * 4;
   const uint32_t cx = crc_of(f.x, nb), cm = crc_of(f.m, nb), cv = crc_of(f.v, nb);
   if (rank == 0) {
-    EXPECT(same_device(f.x, expect.x, nb) && same_device(f.m, expect.m, nb) && same_device(f.v, expect.v, nb),
-           "survivor state != local rw_apply_resolution");
-    free_flat(expect);
+    EXPECT(cx == exp_crc[0] && cm == exp_crc[1] && cv == exp_crc[2], "survivor state != local rw_apply_resolution");
   }
   for (auto& g : markers(f)) EXPECT(g.t == 10 && g.updated == 0, "marker (%llu, %u)", (unsigned long long)g.t, g.updated);
   const auto all_x = gather_u32(c, cx), all_m = gather_u32(c, cm), all_v = gather_u32(c, cv);
