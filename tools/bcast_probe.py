@@ -2,7 +2,6 @@
 under different communicator configs (torchrun, N ranks)."""
 import json
 import os
-import sys
 import time
 
 import torch
