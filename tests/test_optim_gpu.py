@@ -131,6 +131,40 @@ def test_multigroup_bitexact_vs_restatement(restate: Restate, kind, dtype):
             assert np.array_equal(_bits(_get(st, "v", i)), _bits(uv)), i
 
 
+def test_many_groups_beyond_the_presized_slots(restate: Restate):
+    """5,000 ragged groups at 40 distinct t: more work items than a launch slot
+    is pre-sized for at state creation (4,096) and far beyond the inline
+    parameter path (128 items / 16 scalar sets), so the slot grows inside the
+    call; Adam step then undo of every group, bit for bit vs the restatement."""
+    rng = np.random.default_rng(5000)
+    sizes = [int(n) for n in rng.integers(1, 300, 5000)]
+    st = DeviceState(sizes, dtype=torch.float32, kind=ADAM)
+    data = _random_groups(rng, ADAM, sizes, np.float32)
+    t0 = [int(rng.integers(0, 40)) for _ in sizes]
+    flat = {k: np.zeros(st.total, np.float32) for k in "xgmv"}
+    for i, grp in enumerate(data):  # one host image per buffer, one copy each
+        o = st.offsets[i]
+        for k, a in zip("xgmv", grp):
+            flat[k][o:o + sizes[i]] = a
+    for k in "xgmv":
+        getattr(st, k).copy_(torch.from_numpy(flat[k]))
+    st.write_markers([(t, 0) for t in t0])
+    h = HYP[ADAM]
+    st.step(h)
+    st.undo(h)
+    st.check_finite()
+    assert st.markers() == [(t, 0) for t in t0]
+    out = {k: getattr(st, k).cpu().numpy() for k in "xmv"}
+    for i in range(0, len(sizes), 7):  # a deterministic sample of the groups
+        x, g, m, v = data[i]
+        rx, rm, rv, _ = restate.step(ADAM, h, t0[i], x, g, m, v, dtype=np.float32)
+        ux, um, uv, _ = restate.undo(ADAM, h, t0[i] + 1, rx, g, rm, rv, dtype=np.float32)
+        o, n = st.offsets[i], sizes[i]
+        assert np.array_equal(_bits(out["x"][o:o + n]), _bits(ux)), i
+        assert np.array_equal(_bits(out["m"][o:o + n]), _bits(um)), i
+        assert np.array_equal(_bits(out["v"][o:o + n]), _bits(uv)), i
+
+
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 def test_amsgrad_step_bitexact(restate, dtype):
     rng = np.random.default_rng(9)
